@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py -- playouts/s of the batched Da Vinci Code rollout (BASELINE.json
+metric) on 1..8 B200, one process per GPU.
+
+Workload (BASELINE configs[1], the N = 1 headline): C2 = 2 players, 24 tiles,
+mid-game root `fixtures/c2_d1.json`, every legal action x 10^6 playouts per
+action per GPU.  A step = one whole batch of the hot path (SURVEY §8(a) rows
+a1-a5 in the rollout kernel, a6 = NCCL all_reduce of the int64 winner
+histogram when N > 1).  Weak scaling: rank r plays sims [r*n, (r+1)*n) of every
+action, so per-GPU work is fixed and the merged counts are those of N*n sims.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
+on the stream the kernels run on, an L2 flush (256 MiB write) between steps
+outside the events; barrier + synchronize around the timed loop; the max over
+ranks of the summed step time.  `e2e` times the public blocking call with host
+buffers (encode + H2D of the state/actions + kernels + D2H of the histogram).
+`--impl reference` times the oracle (oracle/, scalar C++) on the host cores.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "fixtures/c2_d1.json"
+SIMS_PER_ACTION = 1_000_000
+METRIC = "playouts/sec (1/2/4/8 B200) and warp exec efficiency vs CPU oracle"
+UNIT = "playouts/s"
+
+
+def load_workload(path=WORKLOAD):
+    with open(os.path.join(ROOT, path)) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def instr_per_playout():
+    """Per-unit algorithmic work of the dominant kernel: the
+    thread-instructions per playout of the refill kernel on this workload,
+    from the committed ncu capture (profiles/roofline_unit.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_unit.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_oracle_baseline(d, codes, seed, budget_s=15.0, max_workers=None):
+    """The oracle, as it stands, on the host cores: a bounded sample of the
+    same workload (every action, a contiguous sim slice), one process per
+    core over disjoint sim sub-ranges (SURVEY §8(d) "all cores")."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    cores = max_workers or os.cpu_count() or 1
+    # calibrate on one core
+    t0 = time.perf_counter()
+    n_cal = 200
+    oracle.rollout(d, codes, seed, 0, 0, n_cal)
+    per_playout = (time.perf_counter() - t0) / (n_cal * len(codes))
+    per_core = max(1, int(budget_s / per_playout / len(codes) / 4))   # ~budget/4 wall on all cores
+    n = per_core * cores
+    jobs = [(d, codes, seed, i * per_core, (i + 1) * per_core) for i in range(cores)]
+    with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as ex:
+        list(ex.map(_oracle_job, [(d, codes, seed, 0, 1)] * cores))      # warm the workers
+        t0 = time.perf_counter()
+        list(ex.map(_oracle_job, jobs))
+        dt = time.perf_counter() - t0
+    playouts = n * len(codes)
+    return {"value": playouts / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "%s, all %d actions x sims [0, %d) (%d playouts, %.1f s wall, one oracle process "
+                      "per core over disjoint sim ranges)" % (WORKLOAD, len(codes), n, playouts, dt)}
+
+
+def _oracle_job(args):
+    import oracle
+    d, codes, seed, s0, s1 = args
+    return oracle.rollout(d, codes, seed, 0, s0, s1)
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    d = load_workload()
+    import oracle
+    codes = oracle.legal(d)
+    res = None
+    times = []
+    for step in range(args.warmup + args.steps):
+        r = cpu_oracle_baseline(d, codes, seed=1 + step, budget_s=args.ref_budget)
+        if step >= args.warmup:
+            times.append(r)
+        res = r
+    vals = [r["value"] for r in times]
+    value = sorted(vals)[len(vals) // 2]
+    ms = 1000.0 * (SIMS_PER_ACTION * len(codes)) / value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "C2 mid-game root %s, all %d legal actions, bounded oracle sample per step"
+                       % (WORKLOAD, len(codes)), "sims_per_action": SIMS_PER_ACTION,
+                       "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": "oracle",
+                             "sample": res["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- product arm
+def run_product(args):
+    import torch
+    from paper_2403_10720_b200 import dvc
+
+    ws, rank, local = dist_env()
+    if args.gpus != ws and ws > 1:
+        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, ws), file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    d = load_workload()
+    st = dvc.encode(d)
+    codes = st.legal_actions()
+    A, P = len(codes), st.players
+    n = args.sims
+    s0, s1 = rank * n, (rank + 1) * n
+    if args.kernel == "naive":
+        dvc.set_option("kernel", 1)
+    dvc.set_option("plan_cache", 0)       # plan upload + det table rebuilt inside every step
+    stream = torch.cuda.current_stream()
+    hist = torch.zeros((A, P), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def one_step(seed):
+        hist.zero_()
+        dvc.rollout_batch_async(st, codes, seed, 0, s0, s1, hist, stream=stream)
+        if ws > 1:
+            torch.distributed.all_reduce(hist)
+
+    for w in range(args.warmup):
+        one_step(1000 + w)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    dvc.launch_count(reset=True)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i)                                 # L2 flush, outside the events
+            ev[i][0].record(stream)
+            hist.zero_()
+            kev[i][0].record(stream)
+            dvc.rollout_batch_async(st, codes, 1 + i, 0, s0, s1, hist, stream=stream)
+            kev[i][1].record(stream)
+            if ws > 1:
+                torch.distributed.all_reduce(hist)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = dvc.launch_count(reset=False)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    t = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    t_ms, k_ms = float(t[0]), float(t[1])
+    playouts_per_step = A * n * ws
+    value = playouts_per_step * args.steps / (t_ms / 1000.0)
+    assert int(hist.sum()) == playouts_per_step, "histogram does not account for every playout"
+
+    # ---- e2e through the public blocking API with host buffers
+    e2e = None
+    if ws == 1:
+        dvc.set_option("plan_cache", 0)
+        for w in range(2):
+            dvc.rollout_batch_ex(dvc.encode(d), codes, 50 + w, 0, s0, s1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ke = max(1, args.steps)
+        for i in range(ke):
+            st_i = dvc.encode(d)                               # host encode of the observation
+            h = dvc.rollout_batch_ex(st_i, codes, 1 + i, 0, s0, s1)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        assert int(h.sum()) == A * n
+        e2e = {"value": A * n * ke / dt, "unit": UNIT, "h2d_bytes_per_step": 1024 + 8 * A,
+               "d2h_bytes_per_step": 8 * A * P,
+               "path": "dvc.encode + dvc_rollout_batch_ex (host in/out, blocking)"}
+    else:
+        from paper_2403_10720_b200 import dist as ddist
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            h = ddist.rollout_batch(dvc.encode(d), codes, n * ws, 1 + i)   # returns host int64 [A, P]
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": A * n * ws * args.steps / float(dt[0]), "unit": UNIT,
+               "h2d_bytes_per_step": 1024 + 8 * A, "d2h_bytes_per_step": 8 * A * P,
+               "path": "dvc.encode + dist.rollout_batch (sharded async + NCCL all_reduce + .cpu())"}
+
+    if rank == 0:
+        pk = peaks()
+        unit = instr_per_playout()
+        sm_max = float(pk.get("sm_max_mhz", 1965.0))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # tera thread-instructions / s
+        roof = {"bound": "alu", "peak": peak, "unit": "Tinst/s", "traffic": None,
+                "peak_note": "issue peak = %d SM x 4 SMSP x 32 lanes x %.0f MHz (MEASURED_PEAKS sm_max_mhz)"
+                             % (n_sm, sm_max)}
+        kernel_s = k_ms / 1000.0
+        if unit and unit.get("workload") == WORKLOAD:
+            ipp = float(unit["thread_inst_per_playout"])
+            roof["achieved"] = ipp * A * n / kernel_s / 1e12
+            roof["frac"] = roof["achieved"] / peak
+            roof["per_unit"] = "%.0f thread-instructions per playout (%s)" % (ipp, unit.get("source", ""))
+            roof["traffic"] = unit.get("dram_bytes_per_launch")
+        else:
+            roof["achieved"] = None
+            roof["frac"] = None
+            roof["per_unit"] = "missing profiles/roofline_unit.json"
+        roof["kernel_ms"] = k_ms
+        cpu = None
+        if not args.no_cpu_baseline and ws == 1:
+            try:
+                cpu = cpu_oracle_baseline(d, codes, seed=1, budget_s=args.ref_budget)
+            except Exception as e:  # the baseline must not kill the bench line
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": "failed: %s" % e}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": {"workload": "C2 mid-game root %s (2p, 24 tiles, consecutive), all %d legal actions x "
+                                       "%d playouts per action per GPU" % (WORKLOAD, A, n),
+                           "kernel": args.kernel, "sims_per_action_per_gpu": n, "actions": A,
+                           "l2": "flushed between steps (256 MiB write)", "seeds": "1..K",
+                           "det_table": "rebuilt every step (plan_cache=0)", "parallelism": "sim-range dp%d" % ws},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--kernel", default="refill", choices=["refill", "naive"])
+    ap.add_argument("--sims", type=int, default=SIMS_PER_ACTION)
+    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_product(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

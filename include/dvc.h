@@ -1,0 +1,158 @@
+/*
+ * dvc.h -- C-ABI of libdvc.so: batched Da Vinci Code MCTS rollouts on B200.
+ *
+ * The hot path of arXiv 2403.10720 (BASELINE.json north_star):
+ * for every candidate action at an expanded node, n independent playouts run
+ * to terminal.  Each playout samples a determinization of the opponents'
+ * hidden tiles, applies the action, plays uniformly random
+ * decisions (rules PAPER:102-106, variant PAPER:153) and its winner
+ * is added to integer per-action counts.  The normative
+ * reading of every rule, the RNG contract and the determinization order are in
+ * DESIGN.md §R (= SURVEY.md §8(c)).
+ *
+ * Conventions (all entry points):
+ *  - Status: 0 = DVC_OK; a negative DVC_E_* on failure, with a message in
+ *    dvc_last_error() (thread-local).  A failing call leaves its outputs
+ *    untouched.
+ *  - Ownership: the caller owns every buffer passed in.  The library never
+ *    hands out memory; its per-device scratch (work counters, determinization
+ *    plans and tables, action arrays) is created lazily and freed by
+ *    dvc_shutdown().
+ *  - Host vs device pointers: every pointer is a HOST pointer except the
+ *    d_* arguments of dvc_rollout_batch_async, which are DEVICE pointers on
+ *    `device`.
+ *  - Determinism: outputs are a pure function of (state, action code, seed,
+ *    node_id, sim range); they do not depend on the action-list order, the
+ *    device, the grid/block size, the kernel variant or how the sim range is
+ *    split.
+ *  - No CPU fallback: if no CUDA device is usable, rollout entry points fail
+ *    with DVC_E_CUDA.
+ */
+#ifndef DVC_H_
+#define DVC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DVC_OK = 0,
+  DVC_E_CONFIG = -1,       /* bad rules / params                     */
+  DVC_E_PROTOCOL = -2,     /* not at AwaitGuess / terminal state    */
+  DVC_E_ILLEGAL = -3,      /* an action not in LEGAL(viewer) (+STOP) */
+  DVC_E_INCONSISTENT = -4, /* no consistent determinization / bad tiles  */
+  DVC_E_CAPACITY = -5,     /* caller buffer too small                              */
+  DVC_E_CUDA = -6          /* CUDA error or no device                              */
+};
+
+/* Rules (SPEC:49-53 plus `ranks` for tiny tests).  players 2..4, ranks 1..12,
+ * jokers / consecutive in {0,1}.  consecutive = 1: a correct guess extends the
+ * turn (north_star); 0: the paper's simplification. */
+typedef struct { int32_t players, ranks, jokers, consecutive; } dvc_rules;
+
+/* One tile as the viewer sees it.  color 0 = Black, 1 = White.  value = rank
+ * 0..ranks-1, DVC_JOKER, or DVC_HIDDEN (opponents' hidden tiles only).
+ * revealed = 1 if the tile has been revealed to everybody. */
+#define DVC_JOKER 0xFE
+#define DVC_HIDDEN 0xFF
+typedef struct { uint8_t color, value, revealed, _pad; } dvc_tile_obs;
+
+/* The viewer's information set at AwaitGuess (SPEC:63-68 shape + SURVEY §8(b)).
+ * Lines are seat-indexed and left to right; the viewer's own line is fully
+ * valued.  pending = index in the viewer's line of the tile drawn this turn,
+ * -1 if the pool was empty at turn start.  correct_this_turn >= 1 makes STOP
+ * legal at the root (consecutive rules only). */
+typedef struct {
+  dvc_rules rules;
+  int32_t viewer;
+  int32_t line_len[4];
+  dvc_tile_obs line[4][26];
+  int32_t pool_size, pending, correct_this_turn;
+} dvc_observation;
+
+/* Immutable, pointer-free POD (memcpy/broadcast safe): ranks can build it
+ * independently or ship it byte-for-byte. */
+typedef struct { uint64_t opaque[128]; } dvc_state;
+
+/* Validate an observation and encode it.  Checks, in
+ * order: DVC_E_CONFIG (rules ranges); DVC_E_INCONSISTENT (every tile valid and
+ * at most once, own + revealed + hidden opponent slots + pool_size = |T|, the
+ * viewer's numbered tiles ascending, each opponent's revealed numbered tiles
+ * ascending, N = |Det(O)| >= 1); DVC_E_PROTOCOL (pool_size > 0 => pending >= 0,
+ * pending indexes a hidden viewer tile, correct_this_turn >= 1 => consecutive,
+ * viewer and at least one opponent alive). */
+int dvc_state_encode(const dvc_observation *obs, dvc_state *out);
+
+/* Facts about an encoded state.  n_det = N = |Det(O)|. */
+typedef struct {
+  int32_t players, ranks, jokers, consecutive, viewer, pool_size;
+  int32_t n_legal;          /* |LEGAL(viewer)| + (STOP allowed ? 1 : 0) */
+  int32_t _pad;
+  uint64_t n_det;
+} dvc_state_info;
+int dvc_state_query(const dvc_state *s, dvc_state_info *info);
+
+/* The root's legal action codes in LEGAL order (opponents in
+ * seat order after the viewer, hidden positions left to right, values of the
+ * slot's colour ascending, joker last), then STOP (0xFFFFFFFF) when allowed.
+ * Code = target<<24 | position<<16 | value_key (key = 2*rank+colour; jokers
+ * 2R (black) and 2R+1 (white)).  DVC_E_CAPACITY (and *n_out set) if cap is
+ * too small. */
+#define DVC_STOP 0xFFFFFFFFu
+int dvc_legal_actions(const dvc_state *s, uint32_t *codes, int32_t cap, int32_t *n_out);
+
+/* Root batch, blocking (node_id 0, sims [0, n_sims)): wins[a] = number of the
+ * n_sims playouts of actions[a] won by the viewer.  n_sims in [1, 2^32);
+ * any illegal action fails the whole call (DVC_E_ILLEGAL). */
+int dvc_rollout_batch(const dvc_state *s, const uint32_t *actions, int32_t n_actions,
+                      uint64_t n_sims, uint64_t seed, uint64_t *wins);
+
+/* General blocking form: hist[a*P + w] = #playouts of actions[a] with sim index
+ * in [sim_begin, sim_end) won by seat w (HOST array, overwritten);
+ * visits[a] = sim_end - sim_begin (HOST, may be NULL).  sim_end <= 2^32,
+ * sim_begin < sim_end.  device = CUDA ordinal (-1 = current). */
+int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions,
+                         uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
+                         uint64_t *hist, uint64_t *visits, int32_t device);
+
+/* Asynchronous form: ADDS the counts into the DEVICE arrays d_hist[A*P] (and
+ * d_visits[A] if non-NULL) on `cuda_stream` (a cudaStream_t, NULL = legacy
+ * default stream) of `device`; returns after enqueueing.  The caller zeroes
+ * d_hist when it wants fresh counts.  Host-side state (plan, action arrays) is
+ * staged before return, so the caller may reuse its host buffers at once. */
+int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions,
+                            uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
+                            uint64_t *d_hist, uint64_t *d_visits, int32_t device, void *cuda_stream);
+
+/* Debug/parity form of the async call: additionally writes the winner seat of
+ * every playout to d_winners[a*(sim_end-sim_begin) + (s - sim_begin)] (DEVICE,
+ * uint8).  Same kernels and launch configuration as the async call. */
+int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions,
+                            uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
+                            uint64_t *d_hist, uint8_t *d_winners, int32_t device, void *cuda_stream);
+
+/* Launch options (process-wide; they never change results):
+ *  "kernel"      0 = persistent warp-refill kernel (default), 1 = naive
+ *                thread-per-playout kernel (the paper-style comparison)
+ *  "block"       threads per block (32..1024, multiple of 32; default 256)
+ *  "grid"        blocks (0 = auto: resident blocks per SM x #SM)
+ *  "table_cap"   max determinization-table entries (0 = always unrank inline)
+ *  "plan_cache"  1 = reuse a state's plan + table across calls (default);
+ *                0 = re-upload the plan and rebuild the table on every call
+ * Returns DVC_E_CONFIG for an unknown name or a bad value. */
+int dvc_set_option(const char *name, int64_t value);
+int dvc_get_option(const char *name, int64_t *value);
+
+/* Number of kernel launches the library enqueued since the last reset
+ * (reset = 1 zeroes it); lets callers count GPU launches in a timed region. */
+uint64_t dvc_launch_count(int32_t reset);
+
+const char *dvc_last_error(void);
+void dvc_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DVC_H_ */

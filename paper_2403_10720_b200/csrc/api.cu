@@ -1,0 +1,414 @@
+// api.cu -- the C-ABI of include/dvc.h: argument checks,
+// per-device scratch (work counters, determinization plan + table cache keyed
+// by the state hash), sim-range chunking (<= 2^31 work items per launch so
+// the kernels' u32 counters cannot overflow) and kernel launches.  Every step
+// of the path runs in kernels.cu; this file only marshals.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <list>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "dvc_internal.h"
+#include "rollout.cuh"
+
+namespace dvc {
+cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int grid, int block,
+                           size_t smem, cudaStream_t stream);
+cudaError_t launch_table(const uint8_t *plan, uint64_t N, uint4 *out, cudaStream_t stream);
+cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaStream_t stream);
+cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int block, size_t smem, int *blocks_per_sm);
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_kernel{0}, g_block{256}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1};
+std::atomic<uint64_t> g_launches{0};
+
+int set_err(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+struct PlanEntry {
+  uint64_t hash;
+  uint8_t *d_plan = nullptr;
+  uint4 *d_table = nullptr;   // null if N > table_cap when built
+  uint64_t N = 0;
+  cudaEvent_t ready = nullptr;  // recorded after plan upload + table build
+  std::vector<uint8_t> host_img;
+};
+
+constexpr int kCounterSlots = 4096;
+constexpr size_t kPlanCacheMax = 16;
+
+struct DeviceScratch {
+  int device = -1;
+  int num_sms = 0;
+  uint32_t *d_counters = nullptr;
+  uint32_t next_counter = 0;
+  unsigned long long *d_hist = nullptr;  // blocking calls
+  size_t hist_cap = 0;
+  cudaStream_t stream = nullptr;         // blocking calls
+  std::list<PlanEntry> plans;            // LRU, front = most recent
+};
+
+std::mutex g_mu;
+std::unordered_map<int, DeviceScratch *> g_dev;
+
+int cuda_fail(cudaError_t e, const char *where) {
+  return set_err(DVC_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int get_scratch(int device, DeviceScratch **out) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return set_err(DVC_E_CUDA, "no CUDA device available (no CPU fallback)");
+  if (device < 0) {
+    e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  }
+  if (device >= ndev) return set_err(DVC_E_CONFIG, "device ordinal out of range");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto it = g_dev.find(device);
+  if (it != g_dev.end()) { *out = it->second; return DVC_OK; }
+  DeviceScratch *d = new DeviceScratch();
+  d->device = device;
+  e = cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+  e = cudaMalloc(&d->d_counters, kCounterSlots * sizeof(uint32_t));
+  if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaMalloc(counters)"); }
+  e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { cudaFree(d->d_counters); delete d; return cuda_fail(e, "cudaStreamCreate"); }
+  g_dev[device] = d;
+  *out = d;
+  return DVC_OK;
+}
+
+void free_plan(PlanEntry &p) {
+  if (p.ready) cudaEventSynchronize(p.ready);
+  if (p.d_plan) cudaFree(p.d_plan);
+  if (p.d_table) cudaFree(p.d_table);
+  if (p.ready) cudaEventDestroy(p.ready);
+  p.d_plan = nullptr; p.d_table = nullptr; p.ready = nullptr;
+}
+
+// Plan (+ table) for this state on this device; built on `stream` on first use,
+// other streams wait on its event.
+int get_plan(DeviceScratch *d, const State &st, cudaStream_t stream, PlanEntry **out) {
+  const uint64_t h = ((uint64_t)st.hash_hi << 32) | st.hash_lo;
+  const uint64_t cap = (uint64_t)g_table_cap.load();
+  for (auto it = d->plans.begin(); it != d->plans.end(); ++it) {
+    if (it->hash == h && ((it->d_table != nullptr) == (it->N <= cap))) {
+      d->plans.splice(d->plans.begin(), d->plans, it);
+      PlanEntry &p = d->plans.front();
+      cudaError_t e = cudaStreamWaitEvent(stream, p.ready, 0);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+      if (!g_plan_cache.load()) {
+        // recompute per call (no cross-call reuse): plan upload + table build
+        e = cudaMemcpyAsync(p.d_plan, p.host_img.data(), p.host_img.size(), cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess && p.d_table) {
+          e = launch_table(p.d_plan, p.N, p.d_table, stream);
+          g_launches++;
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(p.ready, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "plan rebuild");
+      }
+      *out = &p;
+      return DVC_OK;
+    }
+  }
+  PlanEntry p;
+  p.hash = h;
+  p.N = build_plan(st, &p.host_img);
+  if (p.N != st.N) return set_err(DVC_E_INCONSISTENT, "determinization count changed (corrupt state?)");
+  cudaError_t e = cudaMalloc(&p.d_plan, p.host_img.size());
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(plan)");
+  e = cudaMemcpyAsync(p.d_plan, p.host_img.data(), p.host_img.size(), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaMemcpyAsync(plan)"); }
+  if (p.N <= cap) {
+    e = cudaMalloc(&p.d_table, p.N * sizeof(uint4));
+    if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaMalloc(table)"); }
+    e = launch_table(p.d_plan, p.N, p.d_table, stream);
+    g_launches++;
+    if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "det_table_kernel"); }
+  }
+  e = cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(p.ready, stream);
+  if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaEventRecord"); }
+  d->plans.push_front(std::move(p));
+  while (d->plans.size() > kPlanCacheMax) {
+    free_plan(d->plans.back());
+    d->plans.pop_back();
+  }
+  *out = &d->plans.front();
+  return DVC_OK;
+}
+
+const State *as_state(const dvc_state *s) {
+  const State *st = reinterpret_cast<const State *>(s);
+  return st->magic == kMagic ? st : nullptr;
+}
+
+// Core enqueue: adds hist for [sim_begin, sim_end) into d_hist on stream.
+int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed, uint32_t node_id,
+            uint64_t sim_begin, uint64_t sim_end, unsigned long long *d_hist, uint8_t *d_winners,
+            int32_t device, cudaStream_t stream, DeviceScratch **dev_out) {
+  const State *st = as_state(s);
+  if (!st) return set_err(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
+  if (!actions || n_actions < 1 || n_actions > kMaxActions)
+    return set_err(DVC_E_CONFIG, "n_actions must be in [1, 768]");
+  if (sim_begin >= sim_end || sim_end > (1ull << 32))
+    return set_err(DVC_E_CONFIG, "need sim_begin < sim_end <= 2^32");
+  KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  const char *err = nullptr;
+  int rc = decode_actions(*st, actions, n_actions, kp.meta, &err);
+  if (rc) return set_err(rc, err ? err : "illegal action");
+  std::memcpy(kp.codes, actions, sizeof(uint32_t) * n_actions);
+
+  std::lock_guard<std::mutex> lock(g_mu);
+  DeviceScratch *d = nullptr;
+  rc = get_scratch(device, &d);
+  if (rc) return rc;
+  if (dev_out) *dev_out = d;
+  PlanEntry *plan = nullptr;
+  rc = get_plan(d, *st, stream, &plan);
+  if (rc) return rc;
+
+  const int P = st->P;
+  kp.k0 = (uint32_t)seed; kp.k1 = (uint32_t)(seed >> 32);
+  kp.node = node_id;
+  kp.A = (uint32_t)n_actions;
+  kp.g0 = (uint32_t)st->viewer;
+  kp.Hv = st->known[st->viewer];
+  kp.V0 = st->V;
+  kp.U = st->U;
+  kp.T = st->T;
+  kp.numm = (1u << (2 * st->R)) - 1u;
+  kp.JB = (uint32_t)(2 * st->R);
+  kp.pend0 = st->pend_key >= 0 ? (uint32_t)st->pend_key : kNoKey;
+  kp.corr0 = (uint32_t)st->corr;
+  kp.N = st->N;
+  kp.table = plan->d_table;
+  kp.plan = plan->d_plan;
+  kp.hist = d_hist;
+  kp.winners = d_winners;
+  kp.trace_stride = (uint32_t)(sim_end - sim_begin);
+  kp.trace_s0 = (uint32_t)sim_begin;
+
+  const int variant = (int)g_kernel.load();
+  const int block = (int)g_block.load();
+  const size_t smem = (size_t)n_actions * P * sizeof(uint32_t);
+  int grid = (int)g_grid.load();
+  if (grid <= 0) {
+    int per_sm = 0;
+    cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, block, smem, &per_sm);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    if (per_sm < 1) return set_err(DVC_E_CONFIG, "kernel cannot launch with this block size");
+    grid = per_sm * d->num_sms;
+  }
+  // chunk the sim range so each launch has <= 2^31 work items
+  const uint64_t per_launch = (1ull << 31) / (uint64_t)n_actions;
+  for (uint64_t b = sim_begin; b < sim_end;) {
+    const uint64_t e_ = (sim_end - b > per_launch) ? b + per_launch : sim_end;
+    kp.s0 = (uint32_t)b;
+    kp.n_per = (uint32_t)(e_ - b);
+    kp.total = kp.n_per * kp.A;
+    kp.counter = d->d_counters + (d->next_counter++ % kCounterSlots);
+    cudaError_t e = cudaMemsetAsync(kp.counter, 0, sizeof(uint32_t), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
+    e = launch_rollout(kp, P, st->jokers != 0, st->consecutive != 0, variant, grid, block, smem, stream);
+    g_launches++;
+    if (e != cudaSuccess) return cuda_fail(e, "rollout kernel launch");
+    b = e_;
+  }
+  return DVC_OK;
+}
+
+}  // namespace
+}  // namespace dvc
+
+using namespace dvc;
+
+extern "C" {
+
+int dvc_state_encode(const dvc_observation *obs, dvc_state *out) {
+  if (!obs || !out) return set_err(DVC_E_CONFIG, "null argument");
+  State st;
+  const char *err = nullptr;
+  int rc = encode(obs, &st, &err);
+  if (rc) return set_err(rc, err ? err : "encode failed");
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out, &st, sizeof(st));
+  return DVC_OK;
+}
+
+int dvc_state_query(const dvc_state *s, dvc_state_info *info) {
+  const State *st = s ? as_state(s) : nullptr;
+  if (!st || !info) return set_err(DVC_E_CONFIG, "bad state");
+  info->players = st->P; info->ranks = st->R; info->jokers = st->jokers;
+  info->consecutive = st->consecutive; info->viewer = st->viewer; info->pool_size = st->pool_size;
+  info->n_legal = st->n_legal; info->_pad = 0; info->n_det = st->N;
+  return DVC_OK;
+}
+
+int dvc_legal_actions(const dvc_state *s, uint32_t *codes, int32_t cap, int32_t *n_out) {
+  const State *st = s ? as_state(s) : nullptr;
+  if (!st || !n_out || (cap > 0 && !codes)) return set_err(DVC_E_CONFIG, "bad arguments");
+  int rc = legal_actions(*st, codes ? codes : nullptr, cap, n_out);
+  if (rc) return set_err(rc, "capacity too small for the legal-action list");
+  return DVC_OK;
+}
+
+int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                         uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
+                         uint64_t *visits, int32_t device) {
+  if (!hist) return set_err(DVC_E_CONFIG, "hist is null");
+  const State *st = s ? as_state(s) : nullptr;
+  if (!st) return set_err(DVC_E_CONFIG, "bad state");
+  if (n_actions < 1 || n_actions > kMaxActions) return set_err(DVC_E_CONFIG, "n_actions must be in [1, 768]");
+  if (!actions) return set_err(DVC_E_CONFIG, "actions is null");
+  if (sim_begin >= sim_end || sim_end > (1ull << 32))
+    return set_err(DVC_E_CONFIG, "need sim_begin < sim_end <= 2^32");
+  {
+    // validate the action list before touching any device (errors leave outputs untouched)
+    std::vector<uint32_t> meta((size_t)n_actions);
+    const char *err = nullptr;
+    int rc = decode_actions(*st, actions, n_actions, meta.data(), &err);
+    if (rc) return set_err(rc, err ? err : "illegal action");
+  }
+  const size_t n = (size_t)n_actions * st->P;
+  DeviceScratch *d = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    int rc = get_scratch(device, &d);
+    if (rc) return rc;
+    if (d->hist_cap < n) {
+      if (d->d_hist) cudaFree(d->d_hist);
+      d->d_hist = nullptr;
+      cudaError_t e = cudaMalloc(&d->d_hist, n * sizeof(unsigned long long));
+      if (e != cudaSuccess) { d->hist_cap = 0; return cuda_fail(e, "cudaMalloc(hist)"); }
+      d->hist_cap = n;
+    }
+    cudaError_t e = cudaMemsetAsync(d->d_hist, 0, n * sizeof(unsigned long long), d->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
+  }
+  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d->d_hist, nullptr, d->device,
+                   d->stream, nullptr);
+  if (rc) return rc;
+  std::vector<unsigned long long> tmp(n);
+  cudaError_t e = cudaMemcpyAsync(tmp.data(), d->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  d->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "rollout");
+  for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
+  if (visits)
+    for (int a = 0; a < n_actions; ++a) visits[a] = sim_end - sim_begin;
+  return DVC_OK;
+}
+
+int dvc_rollout_batch(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t n_sims,
+                      uint64_t seed, uint64_t *wins) {
+  const State *st = s ? as_state(s) : nullptr;
+  if (!st || !wins) return set_err(DVC_E_CONFIG, "bad arguments");
+  if (n_sims == 0 || n_sims >= (1ull << 32)) return set_err(DVC_E_CONFIG, "n_sims must be in [1, 2^32)");
+  if (n_actions < 1 || n_actions > kMaxActions) return set_err(DVC_E_CONFIG, "n_actions must be in [1, 768]");
+  std::vector<uint64_t> hist((size_t)n_actions * st->P);
+  int rc = dvc_rollout_batch_ex(s, actions, n_actions, seed, 0, 0, n_sims, hist.data(), nullptr, -1);
+  if (rc) return rc;
+  for (int a = 0; a < n_actions; ++a) wins[a] = hist[(size_t)a * st->P + st->viewer];
+  return DVC_OK;
+}
+
+int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                            uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
+                            uint64_t *d_visits, int32_t device, void *cuda_stream) {
+  if (!d_hist) return set_err(DVC_E_CONFIG, "d_hist is null");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
+                   reinterpret_cast<unsigned long long *>(d_hist), nullptr, device, stream, nullptr);
+  if (rc) return rc;
+  if (d_visits) {
+    cudaError_t e = launch_add_u64(reinterpret_cast<unsigned long long *>(d_visits), (uint32_t)n_actions,
+                                   sim_end - sim_begin, stream);
+    g_launches++;
+    if (e != cudaSuccess) return cuda_fail(e, "visits");
+  }
+  return DVC_OK;
+}
+
+int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                            uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
+                            uint8_t *d_winners, int32_t device, void *cuda_stream) {
+  if (!d_hist || !d_winners) return set_err(DVC_E_CONFIG, "null device pointer");
+  return enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
+                 reinterpret_cast<unsigned long long *>(d_hist), d_winners, device,
+                 reinterpret_cast<cudaStream_t>(cuda_stream), nullptr);
+}
+
+int dvc_set_option(const char *name, int64_t value) {
+  if (!name) return set_err(DVC_E_CONFIG, "null option name");
+  std::string n(name);
+  if (n == "kernel") {
+    if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "kernel must be 0 (refill) or 1 (naive)");
+    g_kernel = value;
+  } else if (n == "block") {
+    if (value < 32 || value > 1024 || value % 32) return set_err(DVC_E_CONFIG, "block must be 32..1024, multiple of 32");
+    g_block = value;
+  } else if (n == "grid") {
+    if (value < 0 || value > (1 << 20)) return set_err(DVC_E_CONFIG, "grid out of range");
+    g_grid = value;
+  } else if (n == "table_cap") {
+    if (value < 0) return set_err(DVC_E_CONFIG, "table_cap must be >= 0");
+    g_table_cap = value;
+  } else if (n == "plan_cache") {
+    if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "plan_cache must be 0 or 1");
+    g_plan_cache = value;
+  } else {
+    return set_err(DVC_E_CONFIG, "unknown option " + n);
+  }
+  return DVC_OK;
+}
+
+int dvc_get_option(const char *name, int64_t *value) {
+  if (!name || !value) return set_err(DVC_E_CONFIG, "null argument");
+  std::string n(name);
+  if (n == "kernel") *value = g_kernel;
+  else if (n == "block") *value = g_block;
+  else if (n == "grid") *value = g_grid;
+  else if (n == "table_cap") *value = g_table_cap;
+  else if (n == "plan_cache") *value = g_plan_cache;
+  else return set_err(DVC_E_CONFIG, "unknown option " + n);
+  return DVC_OK;
+}
+
+uint64_t dvc_launch_count(int32_t reset) {
+  uint64_t v = g_launches.load();
+  if (reset) g_launches = 0;
+  return v;
+}
+
+const char *dvc_last_error(void) { return g_err.c_str(); }
+
+void dvc_shutdown(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto &kv : g_dev) {
+    DeviceScratch *d = kv.second;
+    cudaSetDevice(d->device);
+    cudaDeviceSynchronize();
+    for (auto &p : d->plans) free_plan(p);
+    if (d->d_counters) cudaFree(d->d_counters);
+    if (d->d_hist) cudaFree(d->d_hist);
+    if (d->stream) cudaStreamDestroy(d->stream);
+    delete d;
+  }
+  g_dev.clear();
+}
+
+}  // extern "C"

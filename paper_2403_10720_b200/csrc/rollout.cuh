@@ -1,0 +1,403 @@
+// rollout.cuh -- device code of the hot path:
+// Philox keyed by (seed; node, action code, sim), canonical
+// determinization by table lookup or inline unranking (§R4), the root action
+// (§R5 APPLY) and the random playout loop (§R5), on 32-bit tile bitmasks held
+// in registers.
+//
+// Seats are kept RELATIVE to the mover: H[0] is the mover's hand, H[d] the
+// hand of the player d seats after it, so LEGAL's "opponents in seat order
+// after g" is a compile-time loop d = 1..P-1 and no register array is ever
+// indexed dynamically.  `g` tracks the mover's absolute seat for the winner.
+#pragma once
+#include <stdint.h>
+#include "dvc_internal.h"
+
+namespace dvc {
+
+constexpr int kMaxActions = 768;
+constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2;
+
+struct KParams {
+  uint32_t k0, k1;        // Philox key = (lo32(seed), hi32(seed))
+  uint32_t node;          // Philox counter word w
+  uint32_t s0;            // first sim index of this launch
+  uint32_t n_per;         // sims per action in this launch
+  uint32_t total;         // A * n_per (<= 2^31)
+  uint32_t A;
+  uint32_t g0;            // viewer seat (mover at the root)
+  uint32_t Hv;            // viewer's hand
+  uint32_t V0;            // revealed keys at the root
+  uint32_t U;             // unaccounted keys (opponents' hidden + pool)
+  uint32_t T;             // tile set
+  uint32_t numm;          // numbered keys mask
+  uint32_t JB;            // 2R (JW = JB + 1)
+  uint32_t pend0, corr0;  // root pending key (kNoKey if none), correct_this_turn
+  uint32_t trace_stride;  // winners[a*trace_stride + (s - trace_s0)]
+  uint32_t trace_s0;
+  uint64_t N;             // |Det(O)|
+  const uint4 *table;     // N entries (H1, H2, H3, jinfo) or null -> inline unrank
+  const uint8_t *plan;    // DetPlanHdr image (inline unrank / table build)
+  unsigned long long *hist;  // [A * P] global counters (added to)
+  uint8_t *winners;       // optional per-playout winner trace
+  uint32_t *counter;      // refill kernel's work counter (zeroed per launch)
+  uint32_t codes[kMaxActions];  // action codes (Philox counter word z)
+  uint32_t meta[kMaxActions];   // act_meta(d, pos, v); d = 0 -> STOP
+};
+
+// ----------------------------------------------------------------- RNG (§R3)
+__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                               uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ uint32_t choose(uint32_t n, uint32_t w) { return __umulhi(w, n); }
+
+__device__ __forceinline__ uint64_t rank64(uint64_t N, uint32_t w0, uint32_t w1) {
+  return __umul64hi(((uint64_t)w1 << 32) | w0, N);
+}
+
+// ----------------------------------------------------------------- bit helpers
+__device__ __forceinline__ uint32_t below(uint32_t k) { return (1u << k) - 1u; }  // k <= 31
+
+// 0-based n-th set bit of m (must exist): fixed 5-step search, no divergence.
+__device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t n) {
+  uint32_t k = 0;
+#pragma unroll
+  for (uint32_t b = 16; b; b >>= 1) {
+    const uint32_t kk = k | b;
+    if ((uint32_t)__popc(m & below(kk)) <= n) k = kk;
+  }
+  return k;
+}
+
+template <int P>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&H)[P], uint32_t d) {
+  uint32_t r = H[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) r = (d == (uint32_t)i) ? H[i] : r;
+  return r;
+}
+
+// ----------------------------------------------------------------- state
+template <int P>
+struct Sim {
+  uint32_t H[P];   // relative seats, H[0] = mover
+  uint32_t V, Q;   // revealed, pool
+  uint32_t ji;     // joker slots (dvc_internal.h jinfo layout)
+  uint32_t g;      // absolute seat of the mover
+  uint32_t pend;   // key drawn this turn or kNoKey
+  uint32_t corr;   // correct guesses this turn
+};
+
+template <int P>
+__device__ __forceinline__ bool over(const Sim<P> &S) {
+  if (P == 2) return !(S.H[0] & ~S.V) || !(S.H[1] & ~S.V);
+  int alive = 0;
+#pragma unroll
+  for (int d = 0; d < P; ++d) alive += (S.H[d] & ~S.V) ? 1 : 0;
+  return alive <= 1;
+}
+
+template <int P>
+__device__ __forceinline__ uint32_t winner_seat(const Sim<P> &S) {
+  uint32_t d = 0;
+#pragma unroll
+  for (int i = P - 1; i >= 1; --i) d = (S.H[i] & ~S.V) ? (uint32_t)i : d;
+  d = (S.H[0] & ~S.V) ? 0u : d;
+  const uint32_t w = S.g + d;
+  return w >= (uint32_t)P ? w - P : w;
+}
+
+// Does the joker `other` (held in the same line) come before joker J?
+__device__ __forceinline__ bool joker_first(uint32_t ji, uint32_t other_is_w, uint32_t s_other,
+                                            uint32_t s_j) {
+  const bool wfirst = (ji >> 10) & 1u;
+  return s_other < s_j || (s_other == s_j && (other_is_w ? wfirst : !wfirst));
+}
+
+// Leftmost hidden tile of hand Hp (DESIGN.md §R5 APPLY).
+template <bool JOK>
+__device__ __forceinline__ uint32_t leftmost_hidden(uint32_t Hp, uint32_t V, uint32_t ji,
+                                                    const KParams &kp) {
+  const uint32_t hid = Hp & ~V;
+  const uint32_t hn = hid & kp.numm;
+  const uint32_t kmin = __ffs(hn) - 1u;
+  if (!JOK) return kmin;
+  const uint32_t hj = (hid >> kp.JB) & 3u;
+  if (!hj) return kmin;
+  // a joker with jslot s precedes the numbered tile of numbered-index r iff s <= r
+  const uint32_t r = hn ? (uint32_t)__popc(Hp & kp.numm & below(kmin)) : 32u;
+  const uint32_t sb = jslot_b(ji), sw = jslot_w(ji);
+  const bool cb = (hj & 1u) && sb <= r;
+  const bool cw = (hj & 2u) && sw <= r;
+  if (cb && cw) return joker_first(ji, 1u, sw, sb) ? kp.JB + 1 : kp.JB;
+  return cb ? kp.JB : (cw ? kp.JB + 1 : kmin);
+}
+
+// 0-based line position of key v held in hand Hp (root action, §R1 "position").
+template <bool JOK>
+__device__ __forceinline__ uint32_t line_pos(uint32_t Hp, uint32_t v, uint32_t ji, const KParams &kp) {
+  const uint32_t sb = jslot_b(ji), sw = jslot_w(ji);
+  if (!JOK || v < kp.JB) {
+    const uint32_t r = __popc(Hp & kp.numm & below(v));
+    uint32_t pos = r;
+    if (JOK) {
+      pos += ((Hp >> kp.JB) & 1u) && sb <= r;
+      pos += ((Hp >> (kp.JB + 1)) & 1u) && sw <= r;
+    }
+    return pos;
+  }
+  const uint32_t is_w = v - kp.JB;            // 0 = JB, 1 = JW
+  const uint32_t s = is_w ? sw : sb, so = is_w ? sb : sw;
+  const bool has_other = (Hp >> (kp.JB + (is_w ^ 1u))) & 1u;
+  return s + ((has_other && joker_first(ji, is_w ^ 1u, so, s)) ? 1u : 0u);
+}
+
+// Insert drawn key t into the mover's hand.
+template <int P, bool JOK>
+__device__ __forceinline__ void insert_drawn(Sim<P> &S, uint32_t t, uint32_t wy, const KParams &kp) {
+  uint32_t H0 = S.H[0];
+  if (JOK) {
+    uint32_t sb = jslot_b(S.ji), sw = jslot_w(S.ji), wf = (S.ji >> 10) & 1u;
+    const bool hasB = (H0 >> kp.JB) & 1u, hasW = (H0 >> (kp.JB + 1)) & 1u;
+    if (t < kp.JB) {
+      // numbered: goes before the first larger numbered tile; jokers of the
+      // mover with jslot > i shift right
+      const uint32_t i = __popc(H0 & kp.numm & below(t));
+      sb += (hasB && sb > i) ? 1u : 0u;
+      sw += (hasW && sw > i) ? 1u : 0u;
+    } else {
+      // joker: uniform gap in [0, len]
+      const uint32_t gam = choose((uint32_t)__popc(H0) + 1u, wy);
+      const uint32_t is_w = t - kp.JB;
+      const bool has_other = is_w ? hasB : hasW;
+      const uint32_t lam = is_w ? sb : sw;       // other joker's line index
+      uint32_t s = gam;
+      bool precedes = true;
+      if (has_other) {
+        precedes = gam <= lam;
+        s = precedes ? gam : gam - 1u;
+        wf = (is_w ? precedes : !precedes) ? 1u : 0u;
+      }
+      if (is_w) sw = s; else sb = s;
+    }
+    S.ji = sb | (sw << 5) | (wf << 10);
+  }
+  S.H[0] = H0 | (1u << t);
+}
+
+// Resolve a guess at the target's tile t with value v (DESIGN.md §R5 APPLY).
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, uint32_t v, const KParams &kp) {
+  if (t == v) {                                      // correct: reveal target
+    S.V |= 1u << t;
+    S.corr += 1;
+    if (over(S)) return FINISH;
+    return CONS ? DECIDE : END_TURN;                 // PAPER:106 vs PAPER:153
+  }
+  // wrong: reveal the mover's drawn tile, else its leftmost hidden
+  const bool pend_hidden = S.pend != kNoKey && !((S.V >> S.pend) & 1u);
+  const uint32_t r = pend_hidden ? S.pend : leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
+  S.V |= 1u << r;
+  return over(S) ? FINISH : END_TURN;
+}
+
+// Hidden tile of opponent hand Hd selected by index x of the mover's LEGAL
+// list restricted to Hd (slots in line order, nB / nW values per black / white
+// slot); returns the tile and the value index inside the slot.
+template <bool JOK>
+__device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji, uint32_t nB,
+                                            uint32_t nW, uint32_t x, const KParams &kp,
+                                            uint32_t *t_out, uint32_t *vidx_out) {
+  const uint32_t hid = Hd & ~V;
+  uint32_t xs = x;
+  if (JOK && ((hid >> kp.JB) & 3u)) {
+    // hidden joker(s) in this line: place them first (rare path)
+    const uint32_t Hn = Hd & kp.numm, cntn = __popc(Hn);
+    const uint32_t hb = hid & kp.numm & kEven, hw = hid & kp.numm & kOdd;
+    const uint32_t sb = jslot_b(ji), sw = jslot_w(ji);
+    const bool hidB = (hid >> kp.JB) & 1u, hidW = (hid >> (kp.JB + 1)) & 1u;
+    uint32_t sel = kNoKey, vidx = 0, sub = 0;
+#pragma unroll
+    for (uint32_t is_w = 0; is_w < 2; ++is_w) {
+      const bool hidJ = is_w ? hidW : hidB;
+      if (!hidJ) continue;
+      const uint32_t s = is_w ? sw : sb;
+      const uint32_t pre = s < cntn ? below(nth_bit(Hn, s)) : kp.numm;
+      uint32_t c = nB * __popc(hb & pre) + nW * __popc(hw & pre);
+      const bool hidO = is_w ? hidB : hidW;
+      const uint32_t so = is_w ? sb : sw;
+      if (hidO && joker_first(ji, is_w ^ 1u, so, s)) c += is_w ? nB : nW;
+      const uint32_t nJ = is_w ? nW : nB;
+      if (x >= c && x < c + nJ) { sel = kp.JB + is_w; vidx = x - c; }
+      else if (x >= c + nJ) sub += nJ;
+    }
+    if (sel != kNoKey) { *t_out = sel; *vidx_out = vidx; return; }
+    xs = x - sub;
+  }
+  const uint32_t hB = hid & kp.numm & kEven, hW = hid & kp.numm & kOdd;
+  uint32_t k = 0, base = 0;
+#pragma unroll
+  for (uint32_t b = 16; b; b >>= 1) {
+    const uint32_t kk = k | b;
+    const uint32_t m = below(kk);
+    const uint32_t c = nB * __popc(hB & m) + nW * __popc(hW & m);
+    if (c <= xs) { k = kk; base = c; }
+  }
+  *t_out = k;
+  *vidx_out = xs - base;
+}
+
+// One decision step (with the turn start it may open).  B = this step's
+// Philox block: B.x pool draw, B.y joker gap, B.z decision.
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ uint32_t step(Sim<P> &S, uint32_t st, uint4 B, const KParams &kp) {
+  if (st == END_TURN) {
+    // next alive player after g becomes the mover (rotate relative seats)
+    if (P == 2) {
+      const uint32_t t0 = S.H[0]; S.H[0] = S.H[1]; S.H[1] = t0;
+      S.g ^= 1u;
+    } else {
+      uint32_t delta = P - 1;
+#pragma unroll
+      for (int d = P - 2; d >= 1; --d) delta = (S.H[d] & ~S.V) ? (uint32_t)d : delta;
+      uint32_t Hn[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        uint32_t v = S.H[(i + 1) % P];
+#pragma unroll
+        for (int dd = 2; dd < P; ++dd) v = (delta == (uint32_t)dd) ? S.H[(i + dd) % P] : v;
+        Hn[i] = v;
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) S.H[i] = Hn[i];
+      S.g += delta;
+      S.g = S.g >= (uint32_t)P ? S.g - P : S.g;
+    }
+    S.pend = kNoKey;
+    S.corr = 0;
+    if (S.Q) {
+      const uint32_t t = nth_bit(S.Q, choose((uint32_t)__popc(S.Q), B.x));
+      S.Q &= ~(1u << t);
+      insert_drawn<P, JOK>(S, t, B.y, kp);
+      S.pend = t;
+    }
+  }
+  // LEGAL(g) size: per hidden opponent slot, the values of its colour that are
+  // neither in the mover's hand nor revealed
+  const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
+  const uint32_t nB = __popc(avail & kEven), nW = __popc(avail & kOdd);
+  uint32_t cnt[P];
+  uint32_t tot = 0;
+#pragma unroll
+  for (int d = 1; d < P; ++d) {
+    const uint32_t hid = S.H[d] & ~S.V;
+    cnt[d] = nB * __popc(hid & kEven) + nW * __popc(hid & kOdd);
+    tot += cnt[d];
+  }
+  const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
+  uint32_t x = choose(n, B.z);
+  if (CONS && x >= tot) return END_TURN;                      // STOP
+  uint32_t d = 1;
+  if (P > 2) {
+    bool found = false;
+#pragma unroll
+    for (int dd = 1; dd < P; ++dd) {
+      const bool here = !found && x < cnt[dd];
+      d = here ? (uint32_t)dd : d;
+      x = (!found && !here) ? x - cnt[dd] : x;
+      found = found || here;
+    }
+  }
+  const uint32_t Hd = pick<P>(S.H, d);
+  uint32_t t, vidx;
+  select_slot<JOK>(Hd, S.V, S.ji, nB, nW, x, kp, &t, &vidx);
+  const uint32_t v = nth_bit(avail & ((t & 1u) ? kOdd : kEven), vidx);
+  return resolve<P, JOK, CONS>(S, t, v, kp);
+}
+
+// ----------------------------------------------------------------- determinization (§R4)
+// rho-th element of Det(O) in canonical order: (H1, H2, H3, jinfo).
+__device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64_t rho) {
+  const DetPlanHdr *hdr = reinterpret_cast<const DetPlanHdr *>(plan);
+  const DetOpt *opts = reinterpret_cast<const DetOpt *>(plan + hdr->opts_off);
+  const uint32_t *slots = reinterpret_cast<const uint32_t *>(plan + hdr->slots_off);
+  const unsigned long long *tab = reinterpret_cast<const unsigned long long *>(plan + hdr->tab_off);
+  const uint32_t n_opts = hdr->n_opts, m = hdr->m, n_opp = hdr->n_opp;
+  uint32_t o = 0;
+  while (o + 1 < n_opts) {
+    const uint64_t c = opts[o].count;
+    if (rho < c) break;
+    rho -= c;
+    ++o;
+  }
+  const DetOpt &op = opts[o];
+  uint32_t hand[3], q[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) { hand[j] = hdr->opp_known[j] | op.jmask[j]; q[j] = 0; }
+  const unsigned long long *T = tab + op.tab_off;
+  const uint32_t ns = op.n_states;
+  uint32_t lin = 0;
+  for (uint32_t i = 0; i < m; ++i) {
+    const uint32_t u = hdr->ukeys[i];
+    const unsigned long long *row = T + (size_t)(i + 1) * ns;
+    uint64_t w = __ldg(row + lin);                 // option: pool
+    if (rho < w) continue;
+    rho -= w;
+#pragma unroll
+    for (uint32_t j = 0; j < 3; ++j) {
+      if (j >= n_opp || q[j] >= op.len[j]) continue;
+      const uint32_t sl = __ldg(slots + op.slot_off[j] + q[j]);
+      const int c = sl & 1u, lo = (int)((sl >> 8) & 0xFFu) - 1, hi = (int)((sl >> 16) & 0xFFu);
+      if ((int)(u & 1u) != c || (int)u <= lo || (int)u >= hi) continue;
+      w = __ldg(row + lin + op.stride[j]);
+      if (rho < w) {
+        hand[j] |= 1u << u;
+        q[j] += 1;
+        lin += op.stride[j];
+        break;
+      }
+      rho -= w;
+    }
+  }
+  return make_uint4(hand[0], hand[1], hand[2], op.jinfo);
+}
+
+// Start playout (a, s): determinize (a2), apply the root action (a3).
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ uint32_t init_playout(Sim<P> &S, uint32_t a, uint32_t s, const KParams &kp) {
+  const uint32_t code = kp.codes[a];
+  const uint4 D = philox4x32_10(0xFFFFFFFFu, s, code, kp.node, kp.k0, kp.k1);
+  const uint64_t rho = rank64(kp.N, D.x, D.y);
+  const uint4 e = kp.table ? __ldg(kp.table + rho) : unrank(kp.plan, rho);
+  S.H[0] = kp.Hv;
+  if (P > 1) S.H[1] = e.x;
+  if (P > 2) S.H[2] = e.y;
+  if (P > 3) S.H[3] = e.z;
+  S.ji = e.w;
+  S.V = kp.V0;
+  uint32_t opp = 0;
+#pragma unroll
+  for (int d = 1; d < P; ++d) opp |= S.H[d];
+  S.Q = kp.U & ~opp;
+  S.g = kp.g0;
+  S.pend = kp.pend0;
+  S.corr = kp.corr0;
+  const uint32_t meta = kp.meta[a];
+  const uint32_t d = meta & 0xFFu;
+  if (d == 0) return END_TURN;                        // STOP
+  const uint32_t pos = (meta >> 8) & 0xFFu, v = meta >> 16;
+  const uint32_t Hd = pick<P>(S.H, d);
+  const bool correct = ((Hd >> v) & 1u) && line_pos<JOK>(Hd, v, S.ji, kp) == pos;
+  return resolve<P, JOK, CONS>(S, correct ? v : kNoKey, v, kp);
+}
+
+}  // namespace dvc

@@ -1,0 +1,42 @@
+"""Root-parallel rollouts across GPUs.
+
+The paper's threads each build a mini-tree from the root and the trees are
+"amalgamated"; merging root statistics is a sum.  Here every rank
+plays the SAME actions on a contiguous slice of every action's sim range,
+[floor(r n / G), floor((r+1) n / G)), and one NCCL all_reduce(SUM) over the
+int64 histogram merges them.  Because playouts are keyed by sim index
+(DESIGN.md §R3), the result is bit-identical for every G.
+
+One process per GPU (torchrun); torch.distributed is plumbing only.
+"""
+
+import torch
+import torch.distributed as dist
+
+from . import dvc
+
+
+def shard_range(n, rank, world):
+    """Contiguous sim sub-range of rank `rank` out of [0, n)."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None, stream=None):
+    """Sharded rollout; returns the merged int64 [A, P] histogram ON DEVICE
+    (every rank holds the same totals after the all_reduce)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    s0, s1 = shard_range(n_sims, rank, world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    hist = torch.zeros((len(actions), state.players), dtype=torch.int64, device=dev)
+    if s1 > s0:
+        dvc.rollout_batch_async(state, actions, seed, node_id, sim_offset + s0, sim_offset + s1, hist,
+                                stream=stream)
+    if world > 1:
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    return hist
+
+
+def rollout_batch(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None):
+    """As rollout_batch_device, read back to host (numpy-compatible int64 tensor)."""
+    return rollout_batch_device(state, actions, n_sims, seed, node_id, sim_offset, group).cpu()

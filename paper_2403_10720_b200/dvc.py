@@ -1,0 +1,257 @@
+"""Thin ctypes binding of libdvc.so (include/dvc.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C-ABI; there is
+no Python or CPU fallback: if libdvc.so is missing, `lib()` raises, and if no
+CUDA device is usable the rollout calls raise DvcError(DVC_E_CUDA).
+PyTorch is used only for device memory and streams (the *_async forms take
+torch CUDA tensors).
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdvc.so")
+
+DVC_OK = 0
+ERRORS = {-1: "DVC_E_CONFIG", -2: "DVC_E_PROTOCOL", -3: "DVC_E_ILLEGAL",
+          -4: "DVC_E_INCONSISTENT", -5: "DVC_E_CAPACITY", -6: "DVC_E_CUDA"}
+STOP = 0xFFFFFFFF
+JOKER = 0xFE
+HIDDEN = 0xFF
+
+# every symbol include/dvc.h declares
+EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
+           "dvc_rollout_batch_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async",
+           "dvc_set_option", "dvc_get_option", "dvc_launch_count", "dvc_last_error", "dvc_shutdown"]
+
+
+class DvcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s (%d): %s" % (ERRORS.get(code, "?"), code, msg))
+        self.code = code
+
+
+class _Rules(ctypes.Structure):
+    _fields_ = [("players", ctypes.c_int32), ("ranks", ctypes.c_int32),
+                ("jokers", ctypes.c_int32), ("consecutive", ctypes.c_int32)]
+
+
+class _TileObs(ctypes.Structure):
+    _fields_ = [("color", ctypes.c_uint8), ("value", ctypes.c_uint8),
+                ("revealed", ctypes.c_uint8), ("_pad", ctypes.c_uint8)]
+
+
+class _Observation(ctypes.Structure):
+    _fields_ = [("rules", _Rules), ("viewer", ctypes.c_int32), ("line_len", ctypes.c_int32 * 4),
+                ("line", (_TileObs * 26) * 4), ("pool_size", ctypes.c_int32),
+                ("pending", ctypes.c_int32), ("correct_this_turn", ctypes.c_int32)]
+
+
+class _State(ctypes.Structure):
+    _fields_ = [("opaque", ctypes.c_uint64 * 128)]
+
+
+class _StateInfo(ctypes.Structure):
+    _fields_ = [("players", ctypes.c_int32), ("ranks", ctypes.c_int32), ("jokers", ctypes.c_int32),
+                ("consecutive", ctypes.c_int32), ("viewer", ctypes.c_int32),
+                ("pool_size", ctypes.c_int32), ("n_legal", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("n_det", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdvc.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libdvc.so not built: run `python -m paper_2403_10720_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, U8, U32, U64, I32, I64 = (ctypes.POINTER, ctypes.c_uint8, ctypes.c_uint32, ctypes.c_uint64,
+                                     ctypes.c_int32, ctypes.c_int64)
+        VP = ctypes.c_void_p
+        L.dvc_state_encode.argtypes = [P(_Observation), P(_State)]
+        L.dvc_state_query.argtypes = [P(_State), P(_StateInfo)]
+        L.dvc_legal_actions.argtypes = [P(_State), P(U32), I32, P(I32)]
+        L.dvc_rollout_batch.argtypes = [P(_State), P(U32), I32, U64, U64, P(U64)]
+        L.dvc_rollout_batch_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, P(U64), P(U64), I32]
+        L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
+        L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
+        L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
+        L.dvc_get_option.argtypes = [ctypes.c_char_p, P(I64)]
+        L.dvc_launch_count.argtypes = [I32]
+        L.dvc_launch_count.restype = U64
+        L.dvc_last_error.restype = ctypes.c_char_p
+        L.dvc_shutdown.restype = None
+        for name in EXPORTS:
+            if name not in ("dvc_launch_count", "dvc_last_error", "dvc_shutdown"):
+                getattr(L, name).restype = I32
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != DVC_OK:
+        raise DvcError(rc, lib().dvc_last_error().decode())
+
+
+def observation(obs_json):
+    """Fixture JSON (SPEC:191 tile shape + pending/correct_this_turn) -> dvc_observation."""
+    o = _Observation()
+    r = obs_json["rules"]
+    o.rules.players = int(r["players"])
+    o.rules.ranks = int(r.get("ranks", 12))
+    o.rules.jokers = int(r.get("jokers", 0))
+    o.rules.consecutive = int(r.get("consecutive", 1))
+    o.viewer = int(obs_json["viewer"])
+    lines = obs_json["lines"]
+    if len(lines) > 4:
+        raise ValueError("at most 4 players")
+    for p, line in enumerate(lines):
+        if len(line) > 26:
+            raise ValueError("line too long")
+        o.line_len[p] = len(line)
+        for i, t in enumerate(line):
+            e = o.line[p][i]
+            e.color = 0 if t["color"] == "B" else 1
+            v = t.get("value")
+            e.value = HIDDEN if v is None else (JOKER if v == "J" else int(v))
+            e.revealed = 1 if t.get("revealed", False) else 0
+    o.pool_size = int(obs_json["pool_size"])
+    o.pending = int(obs_json.get("pending", -1))
+    o.correct_this_turn = int(obs_json.get("correct_this_turn", 0))
+    return o
+
+
+class State:
+    """An encoded root (dvc_state): immutable, pointer-free, picklable bytes."""
+
+    def __init__(self, raw):
+        self._s = raw
+
+    @staticmethod
+    def encode(obs_json):
+        s = _State()
+        _check(lib().dvc_state_encode(ctypes.byref(observation(obs_json)), ctypes.byref(s)))
+        return State(s)
+
+    def to_bytes(self):
+        return bytes(self._s)
+
+    @staticmethod
+    def from_bytes(b):
+        return State(_State.from_buffer_copy(b))
+
+    @property
+    def info(self):
+        i = _StateInfo()
+        _check(lib().dvc_state_query(ctypes.byref(self._s), ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in _StateInfo._fields_ if not k.startswith("_")}
+
+    @property
+    def players(self):
+        return self.info["players"]
+
+    def legal_actions(self):
+        n = ctypes.c_int32()
+        _check(lib().dvc_legal_actions(ctypes.byref(self._s), None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint32 * max(n.value, 1))()
+        _check(lib().dvc_legal_actions(ctypes.byref(self._s), buf, n.value, ctypes.byref(n)))
+        return list(buf[:n.value])
+
+
+def encode(obs_json):
+    return State.encode(obs_json)
+
+
+def _codes(actions):
+    a = np.ascontiguousarray(np.asarray(actions, dtype=np.uint32))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def rollout_batch(state, actions, n_sims, seed):
+    """wins[a] of the viewer over sims [0, n_sims), node 0 (blocking, host output)."""
+    a, ap = _codes(actions)
+    wins = np.zeros(len(a), dtype=np.uint64)
+    _check(lib().dvc_rollout_batch(ctypes.byref(state._s), ap, len(a), n_sims, seed,
+                                   wins.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return wins
+
+
+def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-1):
+    """hist[a, w] (numpy uint64, host) for sims [sim_begin, sim_end) (blocking)."""
+    a, ap = _codes(actions)
+    P = state.players
+    hist = np.zeros((len(a), P), dtype=np.uint64)
+    _check(lib().dvc_rollout_batch_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
+                                      hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), None, device))
+    return hist
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist, visits=None, stream=None):
+    """ADD counts into device tensors hist[A, P] (torch.int64, CUDA) and
+    visits[A] (optional) on `stream` (default: torch's current stream)."""
+    a, ap = _codes(actions)
+    dev = hist.device.index
+    _check(lib().dvc_rollout_batch_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
+                                         ctypes.c_void_p(hist.data_ptr()),
+                                         ctypes.c_void_p(visits.data_ptr()) if visits is not None else None,
+                                         dev, _stream_ptr(stream)))
+
+
+def rollout_trace_async(state, actions, seed, node_id, sim_begin, sim_end, hist, winners, stream=None):
+    """As rollout_batch_async, plus winners[a*(sim_end-sim_begin) + s - sim_begin]
+    (torch.uint8, CUDA) for every playout."""
+    a, ap = _codes(actions)
+    dev = hist.device.index
+    _check(lib().dvc_rollout_trace_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
+                                         ctypes.c_void_p(hist.data_ptr()), ctypes.c_void_p(winners.data_ptr()),
+                                         dev, _stream_ptr(stream)))
+
+
+def set_option(name, value):
+    _check(lib().dvc_set_option(name.encode(), int(value)))
+
+
+def get_option(name):
+    v = ctypes.c_int64()
+    _check(lib().dvc_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
+
+
+class options:
+    """Context manager: temporarily set launch options (they never change results)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_option(k, v)
+
+
+def launch_count(reset=False):
+    return int(lib().dvc_launch_count(1 if reset else 0))
+
+
+def shutdown():
+    lib().dvc_shutdown()
