@@ -52,14 +52,15 @@ class ClockSampler:
 
     def __init__(self, device_index):
         self.dev = device_index
-        self.rows = []
+        self.rows = []          # (t, fields)
         self.proc = None
+        self.window = None      # (t0, t1) of the timed region
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -68,7 +69,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def wait_first(self, timeout=5.0, load=None):
+        """Block (running `load` to keep the GPU busy) until a first sample arrived."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            if load is not None:
+                load()
+            else:
+                time.sleep(0.01)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -79,18 +89,28 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = [r for t, r in self.rows]
+        in_win = rows
+        if self.window is not None:
+            in_win = [r for t, r in self.rows if self.window[0] - 0.06 <= t <= self.window[1] + 0.06]
+        note = "samples inside the timed region"
+        if not in_win:
+            # timed region shorter than the sampling period: the load-phase samples right around it
+            in_win = rows[-3:]
+            note = "timed region shorter than 50 ms sampling: last samples of the same load"
+        rows = in_win
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
-        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        mx = max((float(r[2]) for r in rows if r[2].replace(".", "").isdigit()), default=None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, n in enumerate(names):
                 if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(rows), "note": note}
 
 
 # ----------------------------------------------------------------- helpers
@@ -120,32 +140,48 @@ def instr_per_playout():
         return None
 
 
-def cpu_oracle_baseline(d, codes, seed, budget_s=15.0, max_workers=None):
-    """The oracle, as it stands, on the host cores: a bounded sample of the
-    same workload (every action, a contiguous sim slice), one process per
-    core over disjoint sim sub-ranges (SURVEY §8(d) "all cores")."""
-    from concurrent.futures import ProcessPoolExecutor
-    import multiprocessing as mp
-    import oracle
-    oracle.build()
-    cores = max_workers or os.cpu_count() or 1
-    # calibrate on one core
-    t0 = time.perf_counter()
-    n_cal = 200
-    oracle.rollout(d, codes, seed, 0, 0, n_cal)
-    per_playout = (time.perf_counter() - t0) / (n_cal * len(codes))
-    per_core = max(1, int(budget_s / per_playout / len(codes) / 4))   # ~budget/4 wall on all cores
-    n = per_core * cores
-    jobs = [(d, codes, seed, i * per_core, (i + 1) * per_core) for i in range(cores)]
-    with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as ex:
-        list(ex.map(_oracle_job, [(d, codes, seed, 0, 1)] * cores))      # warm the workers
+class OraclePool:
+    """The oracle, as it stands, on the host cores: one process per core over
+    disjoint sim sub-ranges of the same workload (SURVEY §8(d) "all cores")."""
+
+    def __init__(self, cores=None):
+        from concurrent.futures import ProcessPoolExecutor
+        import multiprocessing as mp
+        import oracle
+        oracle.build()
+        self.cores = cores or os.cpu_count() or 1
+        self.ex = ProcessPoolExecutor(max_workers=self.cores, mp_context=mp.get_context("spawn"))
+
+    def calibrate(self, d, codes, seed, budget_s):
+        """sims per core so one sample takes about budget_s / 4 of wall time."""
+        list(self.ex.map(_oracle_job, [(d, codes, seed, 0, 1)] * self.cores))   # warm the workers
         t0 = time.perf_counter()
-        list(ex.map(_oracle_job, jobs))
+        n_cal = 200
+        list(self.ex.map(_oracle_job, [(d, codes, seed, 0, n_cal)]))
+        per_playout = (time.perf_counter() - t0) / (n_cal * len(codes))
+        return max(1, int(budget_s / per_playout / len(codes) / 4))
+
+    def run(self, d, codes, seed, per_core, offset=0):
+        jobs = [(d, codes, seed, offset + i * per_core, offset + (i + 1) * per_core) for i in range(self.cores)]
+        t0 = time.perf_counter()
+        list(self.ex.map(_oracle_job, jobs))
         dt = time.perf_counter() - t0
-    playouts = n * len(codes)
-    return {"value": playouts / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "%s, all %d actions x sims [0, %d) (%d playouts, %.1f s wall, one oracle process "
-                      "per core over disjoint sim ranges)" % (WORKLOAD, len(codes), n, playouts, dt)}
+        n = per_core * self.cores
+        playouts = n * len(codes)
+        return {"value": playouts / dt, "unit": UNIT, "cores": self.cores, "kind": "oracle",
+                "sample": "%s, all %d actions x %d sims (%d playouts, %.1f s wall, one oracle process per "
+                          "core over disjoint sim ranges)" % (WORKLOAD, len(codes), n, playouts, dt)}
+
+    def close(self):
+        self.ex.shutdown()
+
+
+def cpu_oracle_baseline(d, codes, seed, budget_s=15.0):
+    pool = OraclePool()
+    try:
+        return pool.run(d, codes, seed, pool.calibrate(d, codes, seed, budget_s))
+    finally:
+        pool.close()
 
 
 def _oracle_job(args):
@@ -162,13 +198,16 @@ def run_reference(args):
     d = load_workload()
     import oracle
     codes = oracle.legal(d)
+    pool = OraclePool()
+    per_core = pool.calibrate(d, codes, 1, args.ref_budget / 2)
     res = None
     times = []
     for step in range(args.warmup + args.steps):
-        r = cpu_oracle_baseline(d, codes, seed=1 + step, budget_s=args.ref_budget)
+        r = pool.run(d, codes, seed=1 + step, per_core=per_core)
         if step >= args.warmup:
             times.append(r)
         res = r
+    pool.close()
     vals = [r["value"] for r in times]
     value = sorted(vals)[len(vals) // 2]
     ms = 1000.0 * (SIMS_PER_ACTION * len(codes)) / value
@@ -225,8 +264,14 @@ def run_product(args):
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    dvc.launch_count(reset=True)
     with ClockSampler(local) as clk:
+        clk.wait_first(load=lambda: (one_step(999), torch.cuda.synchronize()))
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        dvc.launch_count(reset=True)
+        t_win0 = time.perf_counter()
         for i in range(args.steps):
             flush.fill_(i)                                 # L2 flush, outside the events
             ev[i][0].record(stream)
@@ -238,7 +283,9 @@ def run_product(args):
                 torch.distributed.all_reduce(hist)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    launches = dvc.launch_count(reset=False)
+        launches = dvc.launch_count(reset=False)
+        clk.window = (t_win0, time.perf_counter())
+        time.sleep(0.06)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()

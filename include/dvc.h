@@ -136,9 +136,12 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
 /* Launch options (process-wide; they never change results):
  *  "kernel"      0 = persistent warp-refill kernel (default), 1 = naive
  *                thread-per-playout kernel (the paper-style comparison)
- *  "block"       threads per block (32..1024, multiple of 32; default 256)
+ *  "block"       threads per block (multiple of 32; 32..1024 for the naive kernel,
+ *                32..256 for the refill kernel; default 128)
  *  "grid"        blocks (0 = auto: resident blocks per SM x #SM)
  *  "table_cap"   max determinization-table entries (0 = always unrank inline)
+ *  "chunk"       max work items (actions x sims) per kernel launch (1..2^31,
+ *                default 2^31; larger ranges are split into several launches)
  *  "plan_cache"  1 = reuse a state's plan + table across calls (default);
  *                0 = re-upload the plan and rebuild the table on every call
  * Returns DVC_E_CONFIG for an unknown name or a bad value. */

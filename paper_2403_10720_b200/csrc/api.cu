@@ -26,7 +26,8 @@ cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int block,
 namespace {
 
 thread_local std::string g_err;
-std::atomic<int64_t> g_kernel{0}, g_block{256}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1};
+std::atomic<int64_t> g_kernel{0}, g_block{128}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1},
+    g_chunk{1ll << 31};
 std::atomic<uint64_t> g_launches{0};
 
 int set_err(int code, const std::string &msg) {
@@ -183,6 +184,10 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
 
   const int P = st->P;
   kp.k0 = (uint32_t)seed; kp.k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    kp.rk[2 * r] = kp.k0 + (uint32_t)r * 0x9E3779B9u;
+    kp.rk[2 * r + 1] = kp.k1 + (uint32_t)r * 0xBB67AE85u;
+  }
   kp.node = node_id;
   kp.A = (uint32_t)n_actions;
   kp.g0 = (uint32_t)st->viewer;
@@ -204,7 +209,9 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
 
   const int variant = (int)g_kernel.load();
   const int block = (int)g_block.load();
-  const size_t smem = (size_t)n_actions * P * sizeof(uint32_t);
+  // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
+  size_t smem = (size_t)n_actions * (P + 2) * sizeof(uint32_t);
+  if (variant == 0) smem += (size_t)(block / 32) * 64 * (P + 7) * sizeof(uint32_t);
   int grid = (int)g_grid.load();
   if (grid <= 0) {
     int per_sm = 0;
@@ -214,12 +221,17 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     grid = per_sm * d->num_sms;
   }
   // chunk the sim range so each launch has <= 2^31 work items
-  const uint64_t per_launch = (1ull << 31) / (uint64_t)n_actions;
+  uint64_t per_launch = (uint64_t)g_chunk.load() / (uint64_t)n_actions;
+  if (per_launch < 1) per_launch = 1;
   for (uint64_t b = sim_begin; b < sim_end;) {
     const uint64_t e_ = (sim_end - b > per_launch) ? b + per_launch : sim_end;
     kp.s0 = (uint32_t)b;
     kp.n_per = (uint32_t)(e_ - b);
     kp.total = kp.n_per * kp.A;
+    kp.nb = (kp.n_per + 63u) / 64u;   // kBatch = 64 (kernels.cu)
+    // ceil(2^64 / n_per) for the kernels' division-free item -> (action, sim)
+    kp.div_magic = kp.n_per == 1 ? 0ull
+                 : (uint64_t)(((unsigned __int128)1 << 64) / kp.n_per) + ((((unsigned __int128)1 << 64) % kp.n_per) ? 1 : 0);
     kp.counter = d->d_counters + (d->next_counter++ % kCounterSlots);
     cudaError_t e = cudaMemsetAsync(kp.counter, 0, sizeof(uint32_t), stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
@@ -367,6 +379,9 @@ int dvc_set_option(const char *name, int64_t value) {
   } else if (n == "table_cap") {
     if (value < 0) return set_err(DVC_E_CONFIG, "table_cap must be >= 0");
     g_table_cap = value;
+  } else if (n == "chunk") {
+    if (value < 1 || value > (1ll << 31)) return set_err(DVC_E_CONFIG, "chunk must be 1..2^31 work items");
+    g_chunk = value;
   } else if (n == "plan_cache") {
     if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "plan_cache must be 0 or 1");
     g_plan_cache = value;
@@ -384,6 +399,7 @@ int dvc_get_option(const char *name, int64_t *value) {
   else if (n == "grid") *value = g_grid;
   else if (n == "table_cap") *value = g_table_cap;
   else if (n == "plan_cache") *value = g_plan_cache;
+  else if (n == "chunk") *value = g_chunk;
   else return set_err(DVC_E_CONFIG, "unknown option " + n);
   return DVC_OK;
 }

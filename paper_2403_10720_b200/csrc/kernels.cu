@@ -21,15 +21,27 @@
 
 namespace dvc {
 
-__device__ __forceinline__ void record(uint32_t *sh_hist, const KParams &kp, uint32_t a, uint32_t s,
-                                       uint32_t w, int P) {
-  atomicAdd(&sh_hist[a * P + w], 1u);
-  if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)w;
-}
+constexpr uint32_t kBatch = 64;   // sims per work batch of the refill kernel
 
-__device__ __forceinline__ void zero_hist(uint32_t *sh, uint32_t n) {
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sh[i] = 0;
+// Shared memory: hist[A*P] u32 counters, then the action codes and metas
+// (read once per playout start; per-lane indexed, so smem beats the param bank).
+struct Smem {
+  uint32_t *hist, *codes, *meta;
+};
+
+__device__ __forceinline__ Smem setup_smem(const KParams &kp, int P) {
+  extern __shared__ uint32_t sh[];
+  Smem m;
+  m.hist = sh;
+  m.codes = sh + kp.A * P;
+  m.meta = m.codes + kp.A;
+  for (uint32_t i = threadIdx.x; i < kp.A * P; i += blockDim.x) m.hist[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kp.A; i += blockDim.x) {
+    m.codes[i] = kp.codes[i];
+    m.meta[i] = kp.meta[i];
+  }
   __syncthreads();
+  return m;
 }
 
 __device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t n, unsigned long long *g) {
@@ -40,80 +52,192 @@ __device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t n, unsig
   }
 }
 
+// Start of playout (a, s): determinization block D, table lookup (a2), root
+// action (a3).  Returns the step state.
 template <int P, bool JOK, bool CONS>
-__global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_constant__ KParams kp) {
-  extern __shared__ uint32_t sh_hist[];
-  zero_hist(sh_hist, kp.A * P);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kp.total; w += stride) {
-    const uint32_t a = w / kp.n_per;
-    const uint32_t s = kp.s0 + (w - a * kp.n_per);
-    const uint32_t code = kp.codes[a];
-    Sim<P> S;
-    uint32_t st = init_playout<P, JOK, CONS>(S, a, s, kp);
-    uint32_t k = 0;
-    while (st != FINISH) {
-      const uint4 B = philox4x32_10(k, s, code, kp.node, kp.k0, kp.k1);
-      st = step<P, JOK, CONS>(S, st, B, kp);
-      ++k;
-    }
-    record(sh_hist, kp, a, s, winner_seat(S), P);
-  }
-  flush_hist(sh_hist, kp.A * P, kp.hist);
+__device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t code, uint32_t meta,
+                                                  const KParams &kp) {
+  const uint4 D = philox_rk(0xFFFFFFFFu, s, code, kp.node, kp);
+  determinize<P>(S, D, kp);
+  uint32_t t;
+  bool correct;
+  const bool stop = root_action<P, JOK>(S, meta, kp, &t, &correct);
+  return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
+}
+
+// Decision step k of a running playout (a4).
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
+                                                 const KParams &kp) {
+  const uint4 B = philox_rk(k, s, code, kp.node, kp);
+  turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
+  uint32_t t;
+  bool correct;
+  const bool stop = decide<P, JOK, CONS>(S, B.z, kp, &t, &correct);
+  return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
 }
 
 template <int P, bool JOK, bool CONS>
-__global__ void __launch_bounds__(1024) rollout_refill_kernel(const __grid_constant__ KParams kp) {
-  extern __shared__ uint32_t sh_hist[];
-  zero_hist(sh_hist, kp.A * P);
+__global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_constant__ KParams kp) {
+  const Smem sm = setup_smem(kp, P);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kp.total; w += stride) {
+    const uint32_t a = div_per(w, kp);
+    const uint32_t s = kp.s0 + (w - a * kp.n_per);
+    const uint32_t code = sm.codes[a], meta = sm.meta[a];
+    Sim<P> S;
+    uint32_t st = start_playout<P, JOK, CONS>(S, s, code, meta, kp);
+    for (uint32_t k = 0; st != FINISH; ++k) st = step_playout<P, JOK, CONS>(S, st, k, s, code, kp);
+    const uint32_t win = winner_seat(S);
+    atomicAdd(&sm.hist[a * P + win], 1u);
+    if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)win;
+  }
+  flush_hist(sm.hist, kp.A * P, kp.hist);
+}
+
+// ---- refill kernel -------------------------------------------------------
+// Every warp keeps a ring of kRing STARTED playouts (determinized, root action
+// applied) in shared memory.  Whenever the ring holds fewer than 32, the whole
+// warp -- converged -- takes 32 new work items and starts them (Philox block D,
+// table lookup, root action), pushing the ones still running.  The main loop is
+// one decision step for every lane; a lane whose playout ends records the
+// winner and pops the next started playout from the ring in the same
+// iteration, so lanes never idle on playout-length variance and the start
+// code never runs with a handful of lanes (BASELINE.json north_star: lanes
+// retire via __ballot_sync and pull new playouts from a work counter).
+constexpr uint32_t kRing = 64;
+
+template <int P>
+struct RingView {
+  uint32_t *base;   // SoA: field f of slot i at base[f * kRing + i]
+  static constexpr int kFields = P + 7;   // H[P], V, Q, ji, packed(g|pend|corr|st), a, s, code
+  __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
+                                      uint32_t code) const {
+#pragma unroll
+    for (int d = 0; d < P; ++d) base[d * kRing + i] = S.H[d];
+    base[(P + 0) * kRing + i] = S.V;
+    base[(P + 1) * kRing + i] = S.Q;
+    base[(P + 2) * kRing + i] = S.ji;
+    base[(P + 3) * kRing + i] = S.g | (S.pend << 2) | (S.corr << 8) | (st << 16);
+    base[(P + 4) * kRing + i] = a;
+    base[(P + 5) * kRing + i] = s;
+    base[(P + 6) * kRing + i] = code;
+  }
+  __device__ __forceinline__ void get(uint32_t i, Sim<P> &S, uint32_t &st, uint32_t &a, uint32_t &s,
+                                      uint32_t &code) const {
+#pragma unroll
+    for (int d = 0; d < P; ++d) S.H[d] = base[d * kRing + i];
+    S.V = base[(P + 0) * kRing + i];
+    S.Q = base[(P + 1) * kRing + i];
+    S.ji = base[(P + 2) * kRing + i];
+    const uint32_t pk = base[(P + 3) * kRing + i];
+    S.g = pk & 3u;
+    S.pend = (pk >> 2) & 31u;
+    S.corr = (pk >> 8) & 0xFFu;
+    st = pk >> 16;
+    a = base[(P + 4) * kRing + i];
+    s = base[(P + 5) * kRing + i];
+    code = base[(P + 6) * kRing + i];
+  }
+};
+
+template <int P, bool JOK, bool CONS>
+__global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_constant__ KParams kp) {
+  const Smem sm = setup_smem(kp, P);
+  extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
+  const RingView<P> ring{sh_all + kp.A * (P + 2) + (threadIdx.x >> 5) * RingView<P>::kFields * kRing};
+  // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
+  // slices of ONE action, so no per-lane division).
+  uint32_t ca = 0, cs = 0, ce = 0, ccode = 0, cmeta = 0;
+  bool drained = false;
+  const uint32_t n_batches = kp.A * kp.nb;
+  uint32_t head = 0, count = 0;       // ring (warp-uniform)
   bool active = false;
-  bool exhausted = false;  // warp-uniform
   uint32_t a = 0, s = 0, code = 0, st = FINISH, k = 0;
   Sim<P> S;
   while (true) {
-    // ---- refill idle lanes from the launch's work counter
-    const uint32_t need = __ballot_sync(0xFFFFFFFFu, !active);
-    if (need && !exhausted) {
-      const uint32_t leader = __ffs(need) - 1u;
-      const uint32_t cnt = __popc(need);
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(kp.counter, cnt);
-      base = __shfl_sync(0xFFFFFFFFu, base, leader);
-      exhausted = base + cnt >= kp.total;
-      if (!active) {
-        const uint32_t w = base + __popc(need & lt_mask);
-        if (w < kp.total) {
-          a = w / kp.n_per;
-          s = kp.s0 + (w - a * kp.n_per);
-          code = kp.codes[a];
-          st = init_playout<P, JOK, CONS>(S, a, s, kp);
-          k = 0;
-          active = true;
-          if (st == FINISH) {
-            record(sh_hist, kp, a, s, winner_seat(S), P);
-            active = false;
-          }
+    // ---- produce: the whole warp starts up to 32 playouts
+    while (count < 32u && !(drained && cs >= ce)) {
+      uint32_t rem = ce - cs;
+      uint32_t na = 0, ns = 0, ne = 0, ncode = 0, nmeta = 0;
+      bool got = false;
+      if (rem < 32u && !drained) {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(kp.counter, 1u);
+        b = __shfl_sync(0xFFFFFFFFu, b, 0);
+        if (b < n_batches) {
+          na = b / kp.nb;
+          ns = (b - na * kp.nb) * kBatch;       // relative to s0 (no u32 overflow at 2^32)
+          ne = min(ns + kBatch, kp.n_per);
+          ncode = sm.codes[na];
+          nmeta = sm.meta[na];
+          got = true;
+        } else {
+          drained = true;
         }
       }
+      bool valid = false;
+      uint32_t pa = 0, ps = 0, pcode = 0, pmeta = 0;
+      if (lane < rem) {
+        pa = ca; ps = kp.s0 + cs + lane; pcode = ccode; pmeta = cmeta; valid = true;
+      } else if (got && ns + (lane - rem) < ne) {
+        pa = na; ps = kp.s0 + ns + (lane - rem); pcode = ncode; pmeta = nmeta; valid = true;
+      }
+      if (got) {
+        ca = na; ccode = ncode; cmeta = nmeta; ce = ne;
+        cs = min(ns + (32u - rem), ne);
+      } else {
+        cs = min(cs + 32u, ce);
+      }
+      Sim<P> T;
+      uint32_t pst = FINISH;
+      if (valid) {
+        pst = start_playout<P, JOK, CONS>(T, ps, pcode, pmeta, kp);
+        if (pst == FINISH) {                    // decided by the root action alone
+          const uint32_t win = winner_seat(T);
+          atomicAdd(&sm.hist[pa * P + win], 1u);
+          if (kp.winners) kp.winners[(size_t)pa * kp.trace_stride + (ps - kp.trace_s0)] = (uint8_t)win;
+          valid = false;
+        }
+      }
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, valid);
+      if (valid) ring.put((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcode);
+      count += __popc(m);
+      __syncwarp();
+    }
+    // ---- idle lanes pop started playouts
+    const uint32_t need = __ballot_sync(0xFFFFFFFFu, !active);
+    if (need && count) {
+      const uint32_t take = min((uint32_t)__popc(need), count);
+      const uint32_t rank = __popc(need & lt_mask);
+      if (!active && rank < take) {
+        ring.get((head + rank) & (kRing - 1u), S, st, a, s, code);
+        k = 0;
+        active = true;
+      }
+      head = (head + take) & (kRing - 1u);
+      count -= take;
+      __syncwarp();
     }
     if (!__any_sync(0xFFFFFFFFu, active)) {
-      if (exhausted) break;
+      if (count == 0 && drained && cs >= ce) break;
       continue;
     }
-    // ---- one decision step for every active lane
+    // ---- one decision step for every running lane
     if (active) {
-      const uint4 B = philox4x32_10(k, s, code, kp.node, kp.k0, kp.k1);
-      st = step<P, JOK, CONS>(S, st, B, kp);
+      st = step_playout<P, JOK, CONS>(S, st, k, s, code, kp);
       ++k;
       if (st == FINISH) {
-        record(sh_hist, kp, a, s, winner_seat(S), P);
+        const uint32_t win = winner_seat(S);
+        atomicAdd(&sm.hist[a * P + win], 1u);
+        if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)win;
         active = false;
       }
     }
   }
-  flush_hist(sh_hist, kp.A * P, kp.hist);
+  flush_hist(sm.hist, kp.A * P, kp.hist);
 }
 
 __global__ void det_table_kernel(const uint8_t *__restrict__ plan, uint64_t N, uint4 *__restrict__ out) {

@@ -35,6 +35,10 @@ struct KParams {
   uint32_t trace_stride;  // winners[a*trace_stride + (s - trace_s0)]
   uint32_t trace_s0;
   uint64_t N;             // |Det(O)|
+  uint64_t div_magic;     // ceil(2^64 / n_per) (0 when n_per == 1): item / n_per = umul64hi(item, magic)
+  uint32_t nb;            // refill kernel: kBatch-sized sim batches per action = ceil(n_per / kBatch)
+  uint32_t rk[20];        // Philox round keys (k0 + r*W0, k1 + r*W1), r = 0..9: read from the
+                          // constant bank as instruction operands (no registers, no adds)
   const uint4 *table;     // N entries (H1, H2, H3, jinfo) or null -> inline unrank
   const uint8_t *plan;    // DetPlanHdr image (inline unrank / table build)
   unsigned long long *hist;  // [A * P] global counters (added to)
@@ -58,10 +62,33 @@ __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   return make_uint4(c0, c1, c2, c3);
 }
 
+// Same function with the batch's precomputed round keys.
+__device__ __forceinline__ uint4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const KParams &kp) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ kp.rk[2 * r], n2 = hi0 ^ c3 ^ kp.rk[2 * r + 1];
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
 __device__ __forceinline__ uint32_t choose(uint32_t n, uint32_t w) { return __umulhi(w, n); }
 
+// floor((w1*2^32 + w0) * N / 2^64).  For N < 2^32 it is exactly
+// (w1*N + hi32(w0*N)) >> 32 (the dropped fraction can never carry).
 __device__ __forceinline__ uint64_t rank64(uint64_t N, uint32_t w0, uint32_t w1) {
+  if ((N >> 32) == 0) {
+    const uint32_t n = (uint32_t)N;
+    return (uint64_t)(((uint64_t)w1 * n + __umulhi(w0, n)) >> 32);
+  }
   return __umul64hi(((uint64_t)w1 << 32) | w0, N);
+}
+
+// item / n_per for item < 2^32, n_per < 2^32 (exact: item * n_per < 2^64).
+__device__ __forceinline__ uint32_t div_per(uint32_t item, const KParams &kp) {
+  return kp.div_magic ? (uint32_t)__umul64hi((uint64_t)item, kp.div_magic) : item;
 }
 
 // ----------------------------------------------------------------- bit helpers
@@ -161,53 +188,81 @@ __device__ __forceinline__ uint32_t line_pos(uint32_t Hp, uint32_t v, uint32_t j
   return s + ((has_other && joker_first(ji, is_w ^ 1u, so, s)) ? 1u : 0u);
 }
 
-// Insert drawn key t into the mover's hand.
+// Turn start (DESIGN.md §R5 END_TURN): the next alive player after g becomes
+// the mover (relative seats rotate), pend/corr reset, and it draws the
+// (choose(|Q|, wx))-th smallest pool key (joker gap from wy).  Written
+// branch-free under the predicate `et` so lanes at different phases of a turn
+// do not diverge; the joker insertion is the only (rare) real branch.
 template <int P, bool JOK>
-__device__ __forceinline__ void insert_drawn(Sim<P> &S, uint32_t t, uint32_t wy, const KParams &kp) {
-  uint32_t H0 = S.H[0];
+__device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t wx, uint32_t wy, const KParams &kp) {
+  if (P == 2) {
+    const uint32_t h0 = et ? S.H[1] : S.H[0], h1 = et ? S.H[0] : S.H[1];
+    S.H[0] = h0; S.H[1] = h1;
+    S.g ^= et ? 1u : 0u;
+  } else {
+    uint32_t delta = P - 1;
+#pragma unroll
+    for (int d = P - 2; d >= 1; --d) delta = (S.H[d] & ~S.V) ? (uint32_t)d : delta;
+    delta = et ? delta : 0u;
+    uint32_t Hn[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      uint32_t v = S.H[i];
+#pragma unroll
+      for (int dd = 1; dd < P; ++dd) v = (delta == (uint32_t)dd) ? S.H[(i + dd) % P] : v;
+      Hn[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) S.H[i] = Hn[i];
+    S.g += delta;
+    S.g = S.g >= (uint32_t)P ? S.g - P : S.g;
+  }
+  const uint32_t t = nth_bit(S.Q, choose((uint32_t)__popc(S.Q), wx));
+  const bool dr = et && S.Q != 0;
+  const uint32_t H0 = S.H[0];
   if (JOK) {
     uint32_t sb = jslot_b(S.ji), sw = jslot_w(S.ji), wf = (S.ji >> 10) & 1u;
     const bool hasB = (H0 >> kp.JB) & 1u, hasW = (H0 >> (kp.JB + 1)) & 1u;
-    if (t < kp.JB) {
-      // numbered: goes before the first larger numbered tile; jokers of the
-      // mover with jslot > i shift right
-      const uint32_t i = __popc(H0 & kp.numm & below(t));
-      sb += (hasB && sb > i) ? 1u : 0u;
-      sw += (hasW && sw > i) ? 1u : 0u;
-    } else {
-      // joker: uniform gap in [0, len]
+    if (dr && t >= kp.JB) {
+      // drawn joker: uniform gap in [0, len]; relative order with the other joker
       const uint32_t gam = choose((uint32_t)__popc(H0) + 1u, wy);
       const uint32_t is_w = t - kp.JB;
       const bool has_other = is_w ? hasB : hasW;
-      const uint32_t lam = is_w ? sb : sw;       // other joker's line index
-      uint32_t s = gam;
-      bool precedes = true;
+      const uint32_t lam = is_w ? sb : sw;
+      uint32_t sj = gam;
       if (has_other) {
-        precedes = gam <= lam;
-        s = precedes ? gam : gam - 1u;
+        const bool precedes = gam <= lam;
+        sj = precedes ? gam : gam - 1u;
         wf = (is_w ? precedes : !precedes) ? 1u : 0u;
       }
-      if (is_w) sw = s; else sb = s;
+      if (is_w) sw = sj; else sb = sj;
+    } else {
+      // numbered: goes before the first larger numbered tile, so the mover's
+      // jokers with jslot > i shift right
+      const uint32_t i = __popc(H0 & kp.numm & below(t));
+      sb += (dr && hasB && sb > i) ? 1u : 0u;
+      sw += (dr && hasW && sw > i) ? 1u : 0u;
     }
     S.ji = sb | (sw << 5) | (wf << 10);
   }
-  S.H[0] = H0 | (1u << t);
+  S.Q = dr ? (S.Q & ~(1u << t)) : S.Q;
+  S.H[0] = dr ? (H0 | (1u << t)) : H0;
+  S.pend = et ? (dr ? t : kNoKey) : S.pend;
+  S.corr = et ? 0u : S.corr;
 }
 
-// Resolve a guess at the target's tile t with value v (DESIGN.md §R5 APPLY).
+// Resolve a guess at a hidden tile t (DESIGN.md §R5 APPLY), branch-free:
+// correct -> reveal t; wrong -> reveal the mover's drawn tile, or
+// its leftmost hidden tile when it drew nothing.
 template <int P, bool JOK, bool CONS>
-__device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, uint32_t v, const KParams &kp) {
-  if (t == v) {                                      // correct: reveal target
-    S.V |= 1u << t;
-    S.corr += 1;
-    if (over(S)) return FINISH;
-    return CONS ? DECIDE : END_TURN;                 // PAPER:106 vs PAPER:153
-  }
-  // wrong: reveal the mover's drawn tile, else its leftmost hidden
+__device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct, const KParams &kp) {
   const bool pend_hidden = S.pend != kNoKey && !((S.V >> S.pend) & 1u);
-  const uint32_t r = pend_hidden ? S.pend : leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
+  const uint32_t lmh = leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
+  const uint32_t r = correct ? t : (pend_hidden ? S.pend : lmh);
   S.V |= 1u << r;
-  return over(S) ? FINISH : END_TURN;
+  S.corr += correct ? 1u : 0u;
+  const uint32_t cont = (CONS && correct) ? DECIDE : END_TURN;   // PAPER:106 vs PAPER:153
+  return over(S) ? FINISH : cont;
 }
 
 // Hidden tile of opponent hand Hd selected by index x of the mover's LEGAL
@@ -256,45 +311,17 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
   *vidx_out = xs - base;
 }
 
-// One decision step (with the turn start it may open).  B = this step's
-// Philox block: B.x pool draw, B.y joker gap, B.z decision.
+// One random decision (DESIGN.md §R5 loop body after the draw): i =
+// choose(n, wz) over LEGAL(g) (+ STOP last).  Returns true for STOP; else the
+// targeted hidden tile t and whether the guessed value equals it.  The value
+// itself is never materialised: the vidx-th available value of t's colour
+// equals t exactly when vidx = #available values of that colour below t.
 template <int P, bool JOK, bool CONS>
-__device__ __forceinline__ uint32_t step(Sim<P> &S, uint32_t st, uint4 B, const KParams &kp) {
-  if (st == END_TURN) {
-    // next alive player after g becomes the mover (rotate relative seats)
-    if (P == 2) {
-      const uint32_t t0 = S.H[0]; S.H[0] = S.H[1]; S.H[1] = t0;
-      S.g ^= 1u;
-    } else {
-      uint32_t delta = P - 1;
-#pragma unroll
-      for (int d = P - 2; d >= 1; --d) delta = (S.H[d] & ~S.V) ? (uint32_t)d : delta;
-      uint32_t Hn[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) {
-        uint32_t v = S.H[(i + 1) % P];
-#pragma unroll
-        for (int dd = 2; dd < P; ++dd) v = (delta == (uint32_t)dd) ? S.H[(i + dd) % P] : v;
-        Hn[i] = v;
-      }
-#pragma unroll
-      for (int i = 0; i < P; ++i) S.H[i] = Hn[i];
-      S.g += delta;
-      S.g = S.g >= (uint32_t)P ? S.g - P : S.g;
-    }
-    S.pend = kNoKey;
-    S.corr = 0;
-    if (S.Q) {
-      const uint32_t t = nth_bit(S.Q, choose((uint32_t)__popc(S.Q), B.x));
-      S.Q &= ~(1u << t);
-      insert_drawn<P, JOK>(S, t, B.y, kp);
-      S.pend = t;
-    }
-  }
-  // LEGAL(g) size: per hidden opponent slot, the values of its colour that are
-  // neither in the mover's hand nor revealed
+__device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t wz, const KParams &kp, uint32_t *t_out,
+                                       bool *correct) {
   const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
-  const uint32_t nB = __popc(avail & kEven), nW = __popc(avail & kOdd);
+  const uint32_t aB = avail & kEven, aW = avail & kOdd;
+  const uint32_t nB = __popc(aB), nW = __popc(aW);
   uint32_t cnt[P];
   uint32_t tot = 0;
 #pragma unroll
@@ -304,8 +331,8 @@ __device__ __forceinline__ uint32_t step(Sim<P> &S, uint32_t st, uint4 B, const 
     tot += cnt[d];
   }
   const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
-  uint32_t x = choose(n, B.z);
-  if (CONS && x >= tot) return END_TURN;                      // STOP
+  uint32_t x = choose(n, wz);
+  const bool stop = CONS && x >= tot;
   uint32_t d = 1;
   if (P > 2) {
     bool found = false;
@@ -320,8 +347,9 @@ __device__ __forceinline__ uint32_t step(Sim<P> &S, uint32_t st, uint4 B, const 
   const uint32_t Hd = pick<P>(S.H, d);
   uint32_t t, vidx;
   select_slot<JOK>(Hd, S.V, S.ji, nB, nW, x, kp, &t, &vidx);
-  const uint32_t v = nth_bit(avail & ((t & 1u) ? kOdd : kEven), vidx);
-  return resolve<P, JOK, CONS>(S, t, v, kp);
+  *t_out = t;
+  *correct = vidx == (uint32_t)__popc(((t & 1u) ? aW : aB) & below(t));
+  return stop;
 }
 
 // ----------------------------------------------------------------- determinization (§R4)
@@ -371,11 +399,9 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
   return make_uint4(hand[0], hand[1], hand[2], op.jinfo);
 }
 
-// Start playout (a, s): determinize (a2), apply the root action (a3).
-template <int P, bool JOK, bool CONS>
-__device__ __forceinline__ uint32_t init_playout(Sim<P> &S, uint32_t a, uint32_t s, const KParams &kp) {
-  const uint32_t code = kp.codes[a];
-  const uint4 D = philox4x32_10(0xFFFFFFFFu, s, code, kp.node, kp.k0, kp.k1);
+// Determinization (a2): state of playout with determinization block D.
+template <int P>
+__device__ __forceinline__ void determinize(Sim<P> &S, uint4 D, const KParams &kp) {
   const uint64_t rho = rank64(kp.N, D.x, D.y);
   const uint4 e = kp.table ? __ldg(kp.table + rho) : unrank(kp.plan, rho);
   S.H[0] = kp.Hv;
@@ -391,13 +417,19 @@ __device__ __forceinline__ uint32_t init_playout(Sim<P> &S, uint32_t a, uint32_t
   S.g = kp.g0;
   S.pend = kp.pend0;
   S.corr = kp.corr0;
-  const uint32_t meta = kp.meta[a];
+}
+
+// The candidate action at the root (a3).  Returns true for STOP; else the
+// guessed key t and whether the target's tile at `pos` is t.
+template <int P, bool JOK>
+__device__ __forceinline__ bool root_action(const Sim<P> &S, uint32_t meta, const KParams &kp, uint32_t *t_out,
+                                            bool *correct) {
   const uint32_t d = meta & 0xFFu;
-  if (d == 0) return END_TURN;                        // STOP
   const uint32_t pos = (meta >> 8) & 0xFFu, v = meta >> 16;
   const uint32_t Hd = pick<P>(S.H, d);
-  const bool correct = ((Hd >> v) & 1u) && line_pos<JOK>(Hd, v, S.ji, kp) == pos;
-  return resolve<P, JOK, CONS>(S, correct ? v : kNoKey, v, kp);
+  *t_out = v;
+  *correct = ((Hd >> v) & 1u) && line_pos<JOK>(Hd, v, S.ji, kp) == pos;
+  return d == 0;
 }
 
 }  // namespace dvc

@@ -101,12 +101,19 @@ def test_schedule_invariance(dvc):
     st = dvc.encode(d)
     codes = st.legal_actions()
     ref = dvc.rollout_batch_ex(st, codes, 11, 0, 0, 30000)
-    configs = [dict(kernel=1), dict(kernel=0, block=32), dict(kernel=0, block=128), dict(kernel=0, grid=1),
-               dict(kernel=0, grid=7), dict(kernel=1, block=1024), dict(kernel=1, grid=3, block=64),
-               dict(table_cap=0), dict(table_cap=0, kernel=1)]
+    configs = [dict(kernel=1), dict(kernel=0, block=32), dict(kernel=0, block=64), dict(kernel=0, block=256),
+               dict(kernel=0, grid=1), dict(kernel=0, grid=7), dict(kernel=1, block=1024),
+               dict(kernel=1, grid=3, block=64), dict(table_cap=0), dict(table_cap=0, kernel=1),
+               dict(chunk=100000), dict(chunk=77777, kernel=1)]
     for cfg in configs:
         with dvc.options(**cfg):
             assert (dvc.rollout_batch_ex(st, codes, 11, 0, 0, 30000) == ref).all(), cfg
+    with dvc.options(kernel=0, block=512):       # beyond the refill kernel's launch bound
+        with pytest.raises(dvc.DvcError):
+            dvc.rollout_batch_ex(st, codes, 11, 0, 0, 100)
+    ref20 = dvc.rollout_batch_ex(st, codes, 11, 0, 0, 20)[:3]
+    with dvc.options(chunk=1, grid=2):            # one sim per launch
+        assert (dvc.rollout_batch_ex(st, codes[:3], 11, 0, 0, 20) == ref20).all()
     # split sim ranges
     parts = [0, 1, 777, 15000, 30000]
     tot = sum(dvc.rollout_batch_ex(st, codes, 11, 0, a, b) for a, b in zip(parts, parts[1:]))
