@@ -21,6 +21,14 @@ def shard_range(n, rank, world):
     return (n * rank) // world, (n * (rank + 1)) // world
 
 
+def merge_hist(hist, group=None):
+    """a6: SUM all-reduce of the per-rank int64 winner histograms (NCCL on CUDA
+    tensors; any torch.distributed backend for the host-side tests)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    return hist
+
+
 def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None, stream=None):
     """Sharded rollout; returns the merged int64 [A, P] histogram ON DEVICE
     (every rank holds the same totals after the all_reduce)."""
@@ -32,9 +40,7 @@ def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, 
     if s1 > s0:
         dvc.rollout_batch_async(state, actions, seed, node_id, sim_offset + s0, sim_offset + s1, hist,
                                 stream=stream)
-    if world > 1:
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
-    return hist
+    return merge_hist(hist, group)
 
 
 def rollout_batch(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None):
