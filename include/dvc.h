@@ -136,9 +136,10 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
 /* Launch options (process-wide; they never change results):
  *  "kernel"      0 = persistent warp-refill kernel (default), 1 = naive
  *                thread-per-playout kernel (the paper-style comparison)
- *  "block"       threads per block (multiple of 32; 32..1024 for the naive kernel,
- *                32..256 for the refill kernel; default 128)
- *  "grid"        blocks (0 = auto: resident blocks per SM x #SM)
+ *  "block"       threads per block (1..1024 for the naive kernel; a multiple of
+ *                32 up to 256 for the refill kernel; default 128)
+ *  "grid"        blocks (0 = auto: resident blocks per SM x #SM, or fewer when
+ *                the launch has less work than that)
  *  "table_cap"   max determinization-table entries (0 = always unrank inline)
  *  "chunk"       max work items (actions x sims) per kernel launch (1..2^31,
  *                default 2^31; larger ranges are split into several launches)
@@ -147,6 +148,32 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
  * Returns DVC_E_CONFIG for an unknown name or a bad value. */
 int dvc_set_option(const char *name, int64_t value);
 int dvc_get_option(const char *name, int64_t *value);
+
+/* Host MCTS over the GPU rollout batches (
+ * PAPER:112-117 four MCTS steps, PAPER:179-186 root-parallel mini-trees).
+ * flat = 1 (the paper's implementation, "expands a child node from
+ * the root, with subsequent gameplay unfolding randomly"): the root's children
+ * are the legal actions; each of `expansions` iterations selects ONE child by
+ * UCB1 (c, IEEE double: wins/visits + c*sqrt(ln(N)/visits), unvisited first,
+ * ties to the smallest code) and runs `sims_per_child` playouts
+ * of it (node 0, sims [visits, visits + n) of that child, so no playout is
+ * ever repeated), then backpropagates visits and the viewer's wins.
+ * flat = 0 is reserved for the depth-capped tree and currently
+ * returns DVC_E_CONFIG.  table[i] receives every root child in LEGAL order
+ * (cap >= n_legal, else DVC_E_CAPACITY); *best_code = most visits, then most
+ * wins, then smallest code. */
+typedef struct {
+  double c;                 /* UCB1 exploration constant (sqrt(2)) */
+  int32_t max_depth;        /* expansion depth threshold (4)       */
+  int32_t expansions;       /* UCB iterations                                 */
+  uint64_t sims_per_child;  /* playouts per iteration                         */
+  uint64_t seed;            /* Philox seed of every batch                     */
+  int32_t flat;             /* 1 = root-only tree                             */
+  int32_t device;           /* CUDA ordinal, -1 = current                     */
+} dvc_search_params;
+typedef struct { uint32_t code, _pad; uint64_t visits, wins; } dvc_action_stat;
+int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table, int32_t cap,
+                    int32_t *n_out, uint32_t *best_code);
 
 /* Number of kernel launches the library enqueued since the last reset
  * (reset = 1 zeroes it); lets callers count GPU launches in a timed region. */

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdvc.so")
-SOURCES = ["api.cu", "kernels.cu", "host.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "host.cpp", "mcts.cpp"]
 HEADERS = ["dvc_internal.h", "rollout.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -56,6 +56,7 @@ struct DeviceScratch {
   size_t hist_cap = 0;
   cudaStream_t stream = nullptr;         // blocking calls
   std::list<PlanEntry> plans;            // LRU, front = most recent
+  std::unordered_map<uint64_t, int> occupancy;   // resident blocks per SM per launch shape
 };
 
 std::mutex g_mu;
@@ -212,13 +213,24 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
   size_t smem = (size_t)n_actions * (P + 2) * sizeof(uint32_t);
   if (variant == 0) smem += (size_t)(block / 32) * 64 * (P + 7) * sizeof(uint32_t);
-  int grid = (int)g_grid.load();
-  if (grid <= 0) {
+  if (variant == 0 && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
+  const int grid_opt = (int)g_grid.load();
+  int grid_full = grid_opt;
+  if (grid_opt <= 0) {
+    // resident blocks per SM, cached per (kernel instance, block, smem)
+    const uint64_t okey = ((uint64_t)variant << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
+                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)block << 32) | (uint64_t)smem;
     int per_sm = 0;
-    cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, block, smem, &per_sm);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    auto it = d->occupancy.find(okey);
+    if (it != d->occupancy.end()) {
+      per_sm = it->second;
+    } else {
+      cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, block, smem, &per_sm);
+      if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+      d->occupancy[okey] = per_sm;
+    }
     if (per_sm < 1) return set_err(DVC_E_CONFIG, "kernel cannot launch with this block size");
-    grid = per_sm * d->num_sms;
+    grid_full = per_sm * d->num_sms;
   }
   // chunk the sim range so each launch has <= 2^31 work items
   uint64_t per_launch = (uint64_t)g_chunk.load() / (uint64_t)n_actions;
@@ -228,13 +240,21 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     kp.s0 = (uint32_t)b;
     kp.n_per = (uint32_t)(e_ - b);
     kp.total = kp.n_per * kp.A;
-    kp.nb = (kp.n_per + 63u) / 64u;   // kBatch = 64 (kernels.cu)
+    kp.nb = (kp.n_per + 31u) / 32u;   // kBatch = 32 (kernels.cu)
     // ceil(2^64 / n_per) for the kernels' division-free item -> (action, sim)
     kp.div_magic = kp.n_per == 1 ? 0ull
                  : (uint64_t)(((unsigned __int128)1 << 64) / kp.n_per) + ((((unsigned __int128)1 << 64) % kp.n_per) ? 1 : 0);
     kp.counter = d->d_counters + (d->next_counter++ % kCounterSlots);
     cudaError_t e = cudaMemsetAsync(kp.counter, 0, sizeof(uint32_t), stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
+    // auto grid: the resident maximum, or fewer blocks for a small launch (each
+    // refill warp starts 32 playouts at a time; each naive thread plays one)
+    int grid = grid_full;
+    if (grid_opt <= 0) {
+      const uint64_t per_block = variant == 0 ? (uint64_t)(block / 32) * 32u : (uint64_t)block;
+      const uint64_t need = ((uint64_t)kp.total + per_block - 1) / per_block;
+      if (need < (uint64_t)grid) grid = (int)need;
+    }
     e = launch_rollout(kp, P, st->jokers != 0, st->consecutive != 0, variant, grid, block, smem, stream);
     g_launches++;
     if (e != cudaSuccess) return cuda_fail(e, "rollout kernel launch");
@@ -244,6 +264,9 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
 }
 
 }  // namespace
+
+int set_error(int code, const char *msg) { return set_err(code, msg ? msg : ""); }
+
 }  // namespace dvc
 
 using namespace dvc;
@@ -371,7 +394,7 @@ int dvc_set_option(const char *name, int64_t value) {
     if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "kernel must be 0 (refill) or 1 (naive)");
     g_kernel = value;
   } else if (n == "block") {
-    if (value < 32 || value > 1024 || value % 32) return set_err(DVC_E_CONFIG, "block must be 32..1024, multiple of 32");
+    if (value < 1 || value > 1024) return set_err(DVC_E_CONFIG, "block must be 1..1024");
     g_block = value;
   } else if (n == "grid") {
     if (value < 0 || value > (1 << 20)) return set_err(DVC_E_CONFIG, "grid out of range");

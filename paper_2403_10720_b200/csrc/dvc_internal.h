@@ -72,6 +72,9 @@ __host__ __device__ inline uint32_t act_meta(uint32_t d, uint32_t pos, uint32_t 
   return d | (pos << 8) | (v << 16);
 }
 
+// ---- error reporting (api.cu): sets dvc_last_error(), returns code ----
+int set_error(int code, const char *msg);
+
 // ---- host functions (host.cpp) ----
 int encode(const dvc_observation *obs, State *st, const char **err);
 int legal_actions(const State &st, uint32_t *codes, int32_t cap, int32_t *n_out);

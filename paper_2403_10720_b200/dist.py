@@ -46,3 +46,42 @@ def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, 
 def rollout_batch(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None):
     """As rollout_batch_device, read back to host (numpy-compatible int64 tensor)."""
     return rollout_batch_device(state, actions, n_sims, seed, node_id, sim_offset, group).cpu()
+
+
+def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, group=None):
+    """Flat root-parallel MCTS on every rank (the tree is replicated: all ranks
+    see the same all-reduced counts, so they make the same UCB1 choices and no
+    tree is ever broadcast).  Each iteration's batch of the selected child is
+    sharded over the ranks' sim ranges (DESIGN.md §R8 / §P).  Same result as
+    dvc_mcts_search on one GPU.  Returns (best_code, [(code, visits, wins)])."""
+    import math
+    codes = state.legal_actions()
+    viewer = state.info["viewer"]
+    visits = [0] * len(codes)
+    wins = [0] * len(codes)
+    N = 0
+    # root expansion: the unvisited children, in ascending code order, as one
+    # leaf-parallel batch (exactly the iterations sequential UCB1 would run)
+    k = min(expansions, len(codes))
+    order = sorted(range(len(codes)), key=lambda a: codes[a])[:k]
+    h = rollout_batch(state, [codes[a] for a in order], sims_per_child, seed, 0, 0, group)
+    for i, a in enumerate(order):
+        visits[a] = sims_per_child
+        wins[a] = int(h[i, viewer])
+        N += sims_per_child
+    for _ in range(expansions - k):
+        best, bv = None, None
+        for a in range(len(codes)):
+            if visits[a] == 0:
+                v = math.inf
+            else:
+                v = wins[a] / visits[a] + c * math.sqrt(math.log(N) / visits[a])
+            if best is None or v > bv or (v == bv and codes[a] < codes[best]):
+                best, bv = a, v
+        h = rollout_batch(state, [codes[best]], sims_per_child, seed, 0, visits[best], group)
+        visits[best] += sims_per_child
+        wins[best] += int(h[0, viewer])
+        N += sims_per_child
+    stats = list(zip(codes, visits, wins))
+    best_code = min(stats, key=lambda t: (-t[1], -t[2], t[0]))[0]
+    return best_code, stats

@@ -24,7 +24,7 @@ HIDDEN = 0xFF
 
 # every symbol include/dvc.h declares
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
-           "dvc_rollout_batch_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async",
+           "dvc_rollout_batch_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async", "dvc_mcts_search",
            "dvc_set_option", "dvc_get_option", "dvc_launch_count", "dvc_last_error", "dvc_shutdown"]
 
 
@@ -52,6 +52,17 @@ class _Observation(ctypes.Structure):
 
 class _State(ctypes.Structure):
     _fields_ = [("opaque", ctypes.c_uint64 * 128)]
+
+
+class _SearchParams(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_double), ("max_depth", ctypes.c_int32), ("expansions", ctypes.c_int32),
+                ("sims_per_child", ctypes.c_uint64), ("seed", ctypes.c_uint64), ("flat", ctypes.c_int32),
+                ("device", ctypes.c_int32)]
+
+
+class _ActionStat(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_uint32), ("_pad", ctypes.c_uint32), ("visits", ctypes.c_uint64),
+                ("wins", ctypes.c_uint64)]
 
 
 class _StateInfo(ctypes.Structure):
@@ -82,6 +93,7 @@ def lib():
         L.dvc_rollout_batch_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, P(U64), P(U64), I32]
         L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
+        L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
         L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
         L.dvc_get_option.argtypes = [ctypes.c_char_p, P(I64)]
         L.dvc_launch_count.argtypes = [I32]
@@ -219,6 +231,20 @@ def rollout_trace_async(state, actions, seed, node_id, sim_begin, sim_end, hist,
     _check(lib().dvc_rollout_trace_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                          ctypes.c_void_p(hist.data_ptr()), ctypes.c_void_p(winners.data_ptr()),
                                          dev, _stream_ptr(stream)))
+
+
+def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, max_depth=4, flat=1, device=-1):
+    """Host UCT over GPU rollout batches (dvc_mcts_search).  Returns
+    (best_code, [(code, visits, wins)] in LEGAL order)."""
+    p = _SearchParams(c=c, max_depth=max_depth, expansions=expansions, sims_per_child=sims_per_child,
+                      seed=seed, flat=flat, device=device)
+    n = ctypes.c_int32()
+    best = ctypes.c_uint32()
+    cap = max(1, state.info["n_legal"])
+    tab = (_ActionStat * cap)()
+    _check(lib().dvc_mcts_search(ctypes.byref(state._s), ctypes.byref(p), tab, cap, ctypes.byref(n),
+                                 ctypes.byref(best)))
+    return best.value, [(t.code, t.visits, t.wins) for t in tab[:n.value]]
 
 
 def set_option(name, value):

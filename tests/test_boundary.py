@@ -116,6 +116,6 @@ def test_options_roundtrip(dvc):
         assert dvc.get_option("block") == 128 and dvc.get_option("kernel") == 1
     assert dvc.get_option("block") == old and dvc.get_option("kernel") == 0
     with pytest.raises(dvc.DvcError):
-        dvc.set_option("block", 33)
+        dvc.set_option("block", 1025)
     with pytest.raises(dvc.DvcError):
         dvc.set_option("nope", 1)

@@ -103,14 +103,16 @@ def test_schedule_invariance(dvc):
     ref = dvc.rollout_batch_ex(st, codes, 11, 0, 0, 30000)
     configs = [dict(kernel=1), dict(kernel=0, block=32), dict(kernel=0, block=64), dict(kernel=0, block=256),
                dict(kernel=0, grid=1), dict(kernel=0, grid=7), dict(kernel=1, block=1024),
-               dict(kernel=1, grid=3, block=64), dict(table_cap=0), dict(table_cap=0, kernel=1),
+               dict(kernel=1, grid=3, block=64), dict(kernel=1, grid=5, block=7), dict(kernel=1, grid=2, block=1),
+               dict(table_cap=0), dict(table_cap=0, kernel=1),
                dict(chunk=100000), dict(chunk=77777, kernel=1)]
     for cfg in configs:
         with dvc.options(**cfg):
             assert (dvc.rollout_batch_ex(st, codes, 11, 0, 0, 30000) == ref).all(), cfg
-    with dvc.options(kernel=0, block=512):       # beyond the refill kernel's launch bound
-        with pytest.raises(dvc.DvcError):
-            dvc.rollout_batch_ex(st, codes, 11, 0, 0, 100)
+    for bad in (512, 48):                         # beyond the launch bound / not whole warps
+        with dvc.options(kernel=0, block=bad):
+            with pytest.raises(dvc.DvcError):
+                dvc.rollout_batch_ex(st, codes, 11, 0, 0, 100)
     ref20 = dvc.rollout_batch_ex(st, codes, 11, 0, 0, 20)[:3]
     with dvc.options(chunk=1, grid=2):            # one sim per launch
         assert (dvc.rollout_batch_ex(st, codes[:3], 11, 0, 0, 20) == ref20).all()
