@@ -117,6 +117,20 @@ int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_
                          uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
                          uint64_t *hist, uint64_t *visits, int32_t device);
 
+/* Deep-tree batch (PAPER:143-170 guess-keyed tree with a
+ * depth threshold): each playout of actions[a] first applies the viewer's
+ * forced actions F = (path[0], ..., path[path_len-1], actions[a]) -- path[0]
+ * as the root action, F[i] at the viewer's i-th later decision (draws and
+ * opponents' decisions stay random) -- then plays randomly to the end.  A
+ * playout whose forced action is illegal in its state, or whose game ends
+ * before all of F is applied, is VOID: counted in voids[a] (HOST, may be NULL),
+ * not in hist.  path[0] must be legal at the root; later codes only
+ * well-formed.  path_len 0..8 (0 = dvc_rollout_batch_ex).  Keys, sims and
+ * node_id as dvc_rollout_batch_ex. */
+int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_len, const uint32_t *actions,
+                        int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
+                        uint64_t *hist, uint64_t *voids, int32_t device);
+
 /* Asynchronous form: ADDS the counts into the DEVICE arrays d_hist[A*P] (and
  * d_visits[A] if non-NULL) on `cuda_stream` (a cudaStream_t, NULL = legacy
  * default stream) of `device`; returns after enqueueing.  The caller zeroes
@@ -158,8 +172,12 @@ int dvc_get_option(const char *name, int64_t *value);
  * ties to the smallest code) and runs `sims_per_child` playouts
  * of it (node 0, sims [visits, visits + n) of that child, so no playout is
  * ever repeated), then backpropagates visits and the viewer's wins.
- * flat = 0 is reserved for the depth-capped tree and currently
- * returns DVC_E_CONFIG.  table[i] receives every root child in LEGAL order
+ * flat = 0: the depth-capped tree over the viewer's guesses (DESIGN.md §R9,
+ * PAPER:143-170; max_depth 1..8): UCB1 descent, expansion of the selected
+ * leaf with ALL its children in one GPU batch (dvc_rollout_path_ex, node_id =
+ * the parent's creation index), re-simulation of leaves at max_depth, void
+ * playouts not counted, backpropagation to the root; `expansions` iterations.
+ * table[i] receives every root child in LEGAL order
  * (cap >= n_legal, else DVC_E_CAPACITY); *best_code = most visits, then most
  * wins, then smallest code. */
 typedef struct {

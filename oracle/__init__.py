@@ -54,6 +54,7 @@ def lib():
         L.oracle_legal.argtypes = [P(I32), P(U32), I32, P(I32)]
         L.oracle_rollout.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64)]
         L.oracle_playout.argtypes = [P(I32), U32, U64, U32, U32, P(I32)]
+        L.oracle_rollout_path.argtypes = [P(I32), P(U32), I32, P(U32), I32, U64, U32, U64, U64, P(U64), P(U64)]
         _lib = L
     return _lib
 
@@ -124,3 +125,17 @@ def playout(obs_json, code, seed, node_id, s):
     st = ctypes.c_int32()
     w = _check(lib().oracle_playout(flatten(obs_json), code, seed, node_id, s, ctypes.byref(st)))
     return w, st.value
+
+
+def rollout_path(obs_json, path, codes, seed, node_id, s0, s1):
+    """Deep-tree batch: (hist[a][w], voids[a]) for forced path + codes[a]."""
+    if not path:
+        return rollout(obs_json, codes, seed, node_id, s0, s1), [0] * len(codes)
+    P = int(obs_json["rules"]["players"])
+    A = len(codes)
+    c = (ctypes.c_uint32 * max(A, 1))(*codes)
+    p = (ctypes.c_uint32 * len(path))(*path)
+    h = (ctypes.c_uint64 * max(A * P, 1))()
+    v = (ctypes.c_uint64 * max(A, 1))()
+    _check(lib().oracle_rollout_path(flatten(obs_json), p, len(path), c, A, seed, node_id, s0, s1, h, v))
+    return [list(h[a * P:(a + 1) * P]) for a in range(A)], list(v[:A])

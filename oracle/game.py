@@ -474,6 +474,48 @@ def playout(space, code, seed, node_id, s, trace=None):
         step = game.apply(a)
 
 
+VOID = "VOID"
+
+
+def playout_path(space, path, code, seed, node_id, s, trace=None):
+    """Deep-tree playout: the viewer's forced actions
+    F = path + [code] -- F[0] at the root, F[i] at the viewer's i-th later
+    decision -- then uniform random play.  Philox keyed by the batch action
+    `code`.  Returns the winner seat, or VOID when a forced action is not in
+    LEGAL (+ STOP when allowed) or the game ends before all of F is applied."""
+    if not path:
+        return playout(space, code, seed, node_id, s, trace)
+    F = list(path) + [code]
+    viewer = space.g0
+    D = px.det_block(seed, node_id, code, s)
+    rho = px.rank64(space.N, D[0], D[1])
+    game = space.game(space.unrank(rho))
+    step = game.apply(F[0])
+    fi = 1
+    k = 0
+    while True:
+        if step == "FINISH":
+            return VOID if fi < len(F) else game.winner()
+        B = px.step_block(seed, node_id, code, s, k)
+        if step == "END_TURN":
+            game.start_turn(B[0], B[1])
+        L = game.legal()
+        n = game.n_choices(L)
+        if fi < len(F) and game.g == viewer:
+            a = F[fi]
+            fi += 1
+            allowed = L + ([STOP] if n > len(L) else [])
+            if a not in allowed:
+                return VOID
+        else:
+            i = px.choose(n, B[2])
+            a = STOP if i == len(L) else L[i]
+        k += 1
+        if trace is not None:
+            trace.append((game.g, a))
+        step = game.apply(a)
+
+
 def check_action(obs, code):
     if code not in root_legal(obs):
         raise ValueError("illegal action %08x" % code)

@@ -391,6 +391,40 @@ int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
   return G.winner();
 }
 
+// Deep-tree playout: forced viewer actions F (F[0] at the
+// root, F[i] at the viewer's i-th later decision), Philox keyed by F.back().
+// Returns the winner, or -1 (VOID) when a forced action is not legal
+// (LEGAL + STOP-when-allowed) or the game ends before all of F is applied.
+int playout_path(DetSpace &sp, const std::vector<u32> &F, u64 seed, u32 node, u32 s, std::vector<u32> &L) {
+  const u32 code = F.back();
+  u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
+  Block D = philox(0xFFFFFFFFu, s, code, node, k0, k1);
+  u64 rho = rank64(sp.N, D.v[0], D.v[1]);
+  Game G = sp.game(sp.unrank(rho));
+  Game::Step st = G.apply(F[0]);
+  size_t fi = 1;
+  u32 k = 0;
+  while (true) {
+    if (st == Game::FINISH) return fi < F.size() ? -1 : G.winner();
+    Block B = philox(k, s, code, node, k0, k1);
+    if (st == Game::END_TURN) G.start_turn(B.v[0], B.v[1]);
+    G.legal(L);
+    const bool stop_ok = G.rules.consecutive && G.corr >= 1;
+    u32 n = (u32)L.size() + (stop_ok ? 1u : 0u);
+    u32 a;
+    if (fi < F.size() && G.g == sp.g0) {
+      a = F[fi++];
+      bool ok = (a == STOP) ? stop_ok : (std::find(L.begin(), L.end(), a) != L.end());
+      if (!ok) return -1;
+    } else {
+      u32 i = choose(n, B.v[2]);
+      a = (i == L.size()) ? STOP : L[i];
+    }
+    k += 1;
+    st = G.apply(a);
+  }
+}
+
 thread_local std::string g_err;
 
 }  // namespace
@@ -446,6 +480,30 @@ int oracle_rollout(const int32_t *obs, const uint32_t *codes, int32_t n_codes, u
     for (int a = 0; a < n_codes; ++a)
       for (u64 s = s0; s < s1; ++s)
         hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L)] += 1;
+    return 0;
+  } catch (std::exception &e) { g_err = e.what(); return -1; }
+}
+
+// deep-tree batch: hist[a*P + w], voids[a] for forced path + codes[a]
+int oracle_rollout_path(const int32_t *obs, const uint32_t *path, int32_t path_len, const uint32_t *codes,
+                        int32_t n_codes, uint64_t seed, uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist,
+                        uint64_t *voids) {
+  try {
+    Obs o = parse(obs);
+    DetSpace sp(o);
+    if (sp.N == 0) { g_err = "inconsistent"; return -4; }
+    std::vector<u32> L;
+    root_legal(o, L);
+    if (path_len < 1 || std::find(L.begin(), L.end(), path[0]) == L.end()) { g_err = "illegal path[0]"; return -3; }
+    int P = o.rules.P;
+    for (int a = 0; a < n_codes; ++a) {
+      std::vector<u32> F(path, path + path_len);
+      F.push_back(codes[a]);
+      for (u64 s = s0; s < s1; ++s) {
+        int w = playout_path(sp, F, seed, node, (u32)s, L);
+        if (w < 0) voids[a] += 1; else hist[(size_t)a * P + w] += 1;
+      }
+    }
     return 0;
   } catch (std::exception &e) { g_err = e.what(); return -1; }
 }

@@ -46,3 +46,75 @@ def flat_search(obs_json, expansions, sims_per_child, seed, c=math.sqrt(2.0)):
         N += sims_per_child
     stats = list(zip(codes, visits, wins))
     return best_child(stats), stats
+
+
+def deep_search(obs_json, expansions, sims_per_child, seed, max_depth=4, c=math.sqrt(2.0)):
+    """Depth-capped tree over the viewer's guesses,
+    written plainly: nodes are dicts; each iteration descends by UCB1, expands
+    the leaf with all candidate children in one batch (or re-simulates a leaf at
+    max_depth), counts non-void playouts and backpropagates them to the root.
+    Returns (best_code, [(code, visits, wins)] of the root's children in LEGAL order)."""
+    from . import rollout_path as oracle_rollout_path
+    root_codes = oracle_legal(obs_json)
+    deep_codes = [x for x in root_codes if x != 0xFFFFFFFF]
+    if obs_json["rules"].get("consecutive", 1):
+        deep_codes.append(0xFFFFFFFF)
+    viewer = obs_json["viewer"]
+    nodes = [{"code": None, "depth": 0, "parent": None, "children": [], "expanded": False,
+              "visits": 0, "wins": 0, "tried": 0}]
+    for _ in range(expansions):
+        # SELECTION
+        x = 0
+        while nodes[x]["expanded"]:
+            best = None
+            for ch in nodes[x]["children"]:
+                node = nodes[ch]
+                if node["tried"] > 0 and node["visits"] == 0:
+                    continue
+                v = math.inf if node["tried"] == 0 else ucb1(node["wins"], node["visits"], nodes[x]["visits"], c)
+                if best is None or v > bv or (v == bv and node["code"] < nodes[best]["code"]):
+                    best, bv = ch, v
+            if best is None:
+                break
+            x = best
+        path = []
+        y = x
+        while y != 0:
+            path.append(nodes[y]["code"])
+            y = nodes[y]["parent"]
+        path.reverse()
+        X = nodes[x]
+        if not X["expanded"] and X["depth"] < max_depth and (x == 0 or X["visits"] > 0):
+            # EXPANSION of every candidate child, evaluated in one batch
+            cand = root_codes if x == 0 else deep_codes
+            evaluated = []
+            for code in cand:
+                nodes.append({"code": code, "depth": X["depth"] + 1, "parent": x, "children": [],
+                              "expanded": False, "visits": 0, "wins": 0, "tried": 0})
+                X["children"].append(len(nodes) - 1)
+                evaluated.append(len(nodes) - 1)
+            X["expanded"] = True
+            prefix, batch, node_word = path, list(cand), x
+        else:
+            if x == 0:
+                break
+            prefix, batch, node_word, evaluated = path[:-1], [X["code"]], X["parent"], [x]
+        s0 = nodes[evaluated[0]]["tried"]
+        # SIMULATION
+        hist, voids = oracle_rollout_path(obs_json, prefix, batch, seed, node_word, s0, s0 + sims_per_child)
+        # BACKPROPAGATION
+        dv = dw = 0
+        for i, e in enumerate(evaluated):
+            nodes[e]["tried"] += sims_per_child
+            nodes[e]["visits"] += sims_per_child - voids[i]
+            nodes[e]["wins"] += hist[i][viewer]
+            dv += sims_per_child - voids[i]
+            dw += hist[i][viewer]
+        y = nodes[evaluated[0]]["parent"]
+        while y is not None:
+            nodes[y]["visits"] += dv
+            nodes[y]["wins"] += dw
+            y = nodes[y]["parent"]
+    by_code = {nodes[ch]["code"]: (nodes[ch]["visits"], nodes[ch]["wins"]) for ch in nodes[0]["children"]}
+    stats = [(code, by_code.get(code, (0, 0))[0], by_code.get(code, (0, 0))[1]) for code in root_codes]
+    return best_child(stats), stats

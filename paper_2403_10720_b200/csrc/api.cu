@@ -21,7 +21,8 @@ cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int va
                            size_t smem, cudaStream_t stream);
 cudaError_t launch_table(const uint8_t *plan, uint64_t N, uint4 *out, cudaStream_t stream);
 cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaStream_t stream);
-cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int block, size_t smem, int *blocks_per_sm);
+cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, bool path, int block, size_t smem,
+                             int *blocks_per_sm);
 
 namespace {
 
@@ -158,9 +159,15 @@ const State *as_state(const dvc_state *s) {
 }
 
 // Core enqueue: adds hist for [sim_begin, sim_end) into d_hist on stream.
+struct PathArg {
+  const uint32_t *codes = nullptr;
+  int32_t len = 0;
+  unsigned long long *d_voids = nullptr;
+};
+
 int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed, uint32_t node_id,
             uint64_t sim_begin, uint64_t sim_end, unsigned long long *d_hist, uint8_t *d_winners,
-            int32_t device, cudaStream_t stream, DeviceScratch **dev_out) {
+            int32_t device, cudaStream_t stream, DeviceScratch **dev_out, const PathArg &path = PathArg()) {
   const State *st = as_state(s);
   if (!st) return set_err(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
   if (!actions || n_actions < 1 || n_actions > kMaxActions)
@@ -170,7 +177,19 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   const char *err = nullptr;
-  int rc = decode_actions(*st, actions, n_actions, kp.meta, &err);
+  int rc;
+  if (path.len > 0) {
+    // deep-tree batch: F[0] = path[0] must be legal at the root; the rest of
+    // the path and the batch actions are applied at later viewer decisions
+    if (path.len > kMaxPath || !path.codes) return set_err(DVC_E_CONFIG, "path length must be 1..8");
+    rc = decode_actions(*st, path.codes, 1, kp.path_meta, &err);
+    if (rc == DVC_OK && path.len > 1) rc = decode_deep(*st, path.codes + 1, path.len - 1, kp.path_meta + 1, &err);
+    if (rc == DVC_OK) rc = decode_deep(*st, actions, n_actions, kp.meta, &err);
+    kp.path_len = (uint32_t)path.len;
+    kp.voids = path.d_voids;
+  } else {
+    rc = decode_actions(*st, actions, n_actions, kp.meta, &err);
+  }
   if (rc) return set_err(rc, err ? err : "illegal action");
   std::memcpy(kp.codes, actions, sizeof(uint32_t) * n_actions);
 
@@ -211,7 +230,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   const int variant = (int)g_kernel.load();
   const int block = (int)g_block.load();
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
-  size_t smem = (size_t)n_actions * (P + 2) * sizeof(uint32_t);
+  size_t smem = ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
   if (variant == 0) smem += (size_t)(block / 32) * 64 * (P + 7) * sizeof(uint32_t);
   if (variant == 0 && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
   const int grid_opt = (int)g_grid.load();
@@ -219,13 +238,15 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   if (grid_opt <= 0) {
     // resident blocks per SM, cached per (kernel instance, block, smem)
     const uint64_t okey = ((uint64_t)variant << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
-                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)block << 32) | (uint64_t)smem;
+                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)(kp.path_len > 0) << 53) |
+                          ((uint64_t)block << 32) | (uint64_t)smem;
     int per_sm = 0;
     auto it = d->occupancy.find(okey);
     if (it != d->occupancy.end()) {
       per_sm = it->second;
     } else {
-      cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, block, smem, &per_sm);
+      cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, kp.path_len > 0, block,
+                                       smem, &per_sm);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy");
       d->occupancy[okey] = per_sm;
     }
@@ -345,6 +366,63 @@ int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_
   for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
   if (visits)
     for (int a = 0; a < n_actions; ++a) visits[a] = sim_end - sim_begin;
+  return DVC_OK;
+}
+
+int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_len, const uint32_t *actions,
+                        int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
+                        uint64_t *hist, uint64_t *voids, int32_t device) {
+  if (path_len == 0) {
+    int rc = dvc_rollout_batch_ex(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device);
+    if (rc == DVC_OK && voids)
+      for (int a = 0; a < n_actions; ++a) voids[a] = 0;
+    return rc;
+  }
+  if (!hist || !actions || !path) return set_err(DVC_E_CONFIG, "null argument");
+  const State *st = s ? as_state(s) : nullptr;
+  if (!st) return set_err(DVC_E_CONFIG, "bad state");
+  if (n_actions < 1 || n_actions > kMaxActions) return set_err(DVC_E_CONFIG, "n_actions must be in [1, 768]");
+  if (path_len < 0 || path_len > kMaxPath) return set_err(DVC_E_CONFIG, "path length must be 0..8");
+  if (sim_begin >= sim_end || sim_end > (1ull << 32)) return set_err(DVC_E_CONFIG, "need sim_begin < sim_end <= 2^32");
+  {
+    std::vector<uint32_t> meta((size_t)(n_actions > path_len ? n_actions : path_len));
+    const char *err = nullptr;
+    int rc = decode_actions(*st, path, 1, meta.data(), &err);
+    if (rc == DVC_OK && path_len > 1) rc = decode_deep(*st, path + 1, path_len - 1, meta.data(), &err);
+    if (rc == DVC_OK) rc = decode_deep(*st, actions, n_actions, meta.data(), &err);
+    if (rc) return set_err(rc, err ? err : "illegal action");
+  }
+  const size_t n = (size_t)n_actions * st->P;
+  DeviceScratch *d = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    int rc = get_scratch(device, &d);
+    if (rc) return rc;
+    if (d->hist_cap < n + (size_t)n_actions) {
+      if (d->d_hist) cudaFree(d->d_hist);
+      d->d_hist = nullptr;
+      cudaError_t e = cudaMalloc(&d->d_hist, (n + n_actions) * sizeof(unsigned long long));
+      if (e != cudaSuccess) { d->hist_cap = 0; return cuda_fail(e, "cudaMalloc(hist)"); }
+      d->hist_cap = n + n_actions;
+    }
+    cudaError_t e = cudaMemsetAsync(d->d_hist, 0, (n + n_actions) * sizeof(unsigned long long), d->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
+  }
+  PathArg pa;
+  pa.codes = path;
+  pa.len = path_len;
+  pa.d_voids = d->d_hist + n;
+  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d->d_hist, nullptr, d->device,
+                   d->stream, nullptr, pa);
+  if (rc) return rc;
+  std::vector<unsigned long long> tmp(n + n_actions);
+  cudaError_t e = cudaMemcpyAsync(tmp.data(), d->d_hist, tmp.size() * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, d->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "rollout");
+  for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
+  if (voids)
+    for (int a = 0; a < n_actions; ++a) voids[a] = tmp[n + a];
   return DVC_OK;
 }
 

@@ -23,6 +23,7 @@ constexpr uint32_t kOdd = 0xAAAAAAAAu;    // white keys (incl. JW = 2R+1)
 constexpr uint32_t kNoKey = 31u;          // "NONE" for pend
 constexpr uint8_t kHiddenSlot = 0x80u;    // line[][] entry flag: hidden, low bit = colour
 constexpr int kMaxOpts = 256;             // joint joker options (<= 14*14 in practice)
+constexpr int kMaxPath = 8;               // deep-tree batches: forced viewer actions before the batch action
 
 // jinfo word: jslot(JB) in bits [0,5), jslot(JW) in [5,10), bit 10 = JW precedes
 // JB when both sit in one line (only read when their jslots are equal).
@@ -81,6 +82,8 @@ int legal_actions(const State &st, uint32_t *codes, int32_t cap, int32_t *n_out)
 // validates codes against LEGAL; fills meta[] for the kernel
 int decode_actions(const State &st, const uint32_t *codes, int32_t n, uint32_t *meta,
                    const char **err);
+// structural validation of deep-tree path / batch codes (legality is per playout)
+int decode_deep(const State &st, const uint32_t *codes, int32_t n, uint32_t *meta, const char **err);
 // builds the plan image into `img` (resized); returns N
 uint64_t build_plan(const State &st, std::vector<uint8_t> *img);
 

@@ -193,6 +193,27 @@ int decode_actions(const State &s, const uint32_t *codes, int32_t n, uint32_t *m
   return DVC_OK;
 }
 
+// Codes applied at the viewer's later decisions of a deep-tree batch
+// (DESIGN.md §R9): only structurally valid here; legality is decided per
+// playout (an illegal one voids the playout).
+int decode_deep(const State &s, const uint32_t *codes, int32_t n, uint32_t *meta, const char **err) {
+  for (int a = 0; a < n; ++a) {
+    uint32_t c = codes[a];
+    if (c == DVC_STOP) {
+      if (!s.consecutive) { fail(err, "STOP can never be legal without consecutive rules"); return DVC_E_ILLEGAL; }
+      meta[a] = 0;
+      continue;
+    }
+    int j = (int)(c >> 24), pos = (int)((c >> 16) & 0xFF), v = (int)(c & 0xFFFF);
+    if (j >= s.P || j == s.viewer || pos >= 26 || v >= 32 || !(s.T & bit(v))) {
+      fail(err, "malformed action code in a deep-tree path");
+      return DVC_E_ILLEGAL;
+    }
+    meta[a] = act_meta((uint32_t)((j - s.viewer + s.P) % s.P), (uint32_t)pos, (uint32_t)v);
+  }
+  return DVC_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Determinization plan (DESIGN.md §R4 reference algorithm, bitmask form).
 namespace {

@@ -25,59 +25,94 @@ constexpr uint32_t kBatch = 32;   // sims per work batch of the refill kernel (o
 
 // Shared memory: hist[A*P] u32 counters, then the action codes and metas
 // (read once per playout start; per-lane indexed, so smem beats the param bank).
+// hist has P + 1 columns: column P counts void playouts (deep-tree batches).
 struct Smem {
-  uint32_t *hist, *codes, *meta;
+  uint32_t *hist, *codes, *meta, *path;
 };
 
 __device__ __forceinline__ Smem setup_smem(const KParams &kp, int P) {
   extern __shared__ uint32_t sh[];
   Smem m;
   m.hist = sh;
-  m.codes = sh + kp.A * P;
+  m.codes = sh + kp.A * (P + 1);
   m.meta = m.codes + kp.A;
-  for (uint32_t i = threadIdx.x; i < kp.A * P; i += blockDim.x) m.hist[i] = 0;
+  m.path = m.meta + kp.A;
+  for (uint32_t i = threadIdx.x; i < kp.A * (P + 1); i += blockDim.x) m.hist[i] = 0;
   for (uint32_t i = threadIdx.x; i < kp.A; i += blockDim.x) {
     m.codes[i] = kp.codes[i];
     m.meta[i] = kp.meta[i];
   }
+  if (threadIdx.x < (uint32_t)kMaxPath) m.path[threadIdx.x] = kp.path_meta[threadIdx.x];
   __syncthreads();
   return m;
 }
 
-__device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t n, unsigned long long *g) {
+__device__ __forceinline__ void flush_hist(const uint32_t *sh, const KParams &kp, int P) {
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (uint32_t i = threadIdx.x; i < kp.A * (P + 1); i += blockDim.x) {
     const uint32_t v = sh[i];
-    if (v) atomicAdd(g + i, (unsigned long long)v);
+    if (!v) continue;
+    const uint32_t a = i / (P + 1), w = i - a * (P + 1);
+    if (w < (uint32_t)P) atomicAdd(kp.hist + a * P + w, (unsigned long long)v);
+    else if (kp.voids) atomicAdd(kp.voids + a, (unsigned long long)v);
   }
+}
+
+// Winner column of a finished playout: its seat, or P for a void deep-tree
+// playout (a forced action was illegal, or the game ended before all forced
+// viewer actions were applied).
+template <int P, bool PATH>
+__device__ __forceinline__ uint32_t outcome(const Sim<P> &S, uint32_t st, const KParams &kp) {
+  if (!PATH) return winner_seat(S);
+  return (st == VOID || S.fi <= kp.path_len) ? (uint32_t)P : winner_seat(S);
+}
+
+__device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P, uint32_t a, uint32_t s,
+                                       uint32_t w) {
+  atomicAdd(&sm.hist[a * (P + 1) + w], 1u);
+  if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)w;
 }
 
 // Start of playout (a, s): determinization block D, table lookup (a2), root
 // action (a3).  Returns the step state.
-template <int P, bool JOK, bool CONS>
+template <int P, bool JOK, bool CONS, bool PATH>
 __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t code, uint32_t meta,
                                                   const KParams &kp) {
   const uint4 D = philox_rk(0xFFFFFFFFu, s, code, kp.node, kp);
   determinize<P>(S, D, kp);
   uint32_t t;
   bool correct;
-  const bool stop = root_action<P, JOK>(S, meta, kp, &t, &correct);
+  // deep-tree batches apply the path's first action at the root (F[0])
+  const bool stop = root_action<P, JOK>(S, PATH ? kp.path_meta[0] : meta, kp, &t, &correct);
+  if (PATH) S.fi = 1;
   return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
 }
 
 // Decision step k of a running playout (a4).
-template <int P, bool JOK, bool CONS>
+template <int P, bool JOK, bool CONS, bool PATH>
 __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
+                                                 const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                  const KParams &kp) {
   const uint4 B = philox_rk(k, s, code, kp.node, kp);
   turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
   uint32_t t;
   bool correct;
-  const bool stop = decide<P, JOK, CONS>(S, B.z, kp, &t, &correct);
+  bool stop;
+  if (PATH && S.fi <= kp.path_len && S.g == kp.g0) {
+    // deep-tree batch: the viewer's next forced action F[fi] (the batch
+    // action itself at fi == path_len) replaces the random decision
+    const uint32_t m = S.fi < kp.path_len ? path_of[S.fi] : meta_of_a[a];
+    bool illegal;
+    stop = forced_decide<P, JOK, CONS>(S, m, kp, &t, &correct, &illegal);
+    S.fi += 1;
+    if (illegal) return VOID;
+  } else {
+    stop = decide<P, JOK, CONS>(S, B.z, kp, &t, &correct);
+  }
   return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
 }
 
-template <int P, bool JOK, bool CONS>
+template <int P, bool JOK, bool CONS, bool PATH>
 __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_constant__ KParams kp) {
   const Smem sm = setup_smem(kp, P);
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -86,13 +121,12 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
     const uint32_t s = kp.s0 + (w - a * kp.n_per);
     const uint32_t code = sm.codes[a], meta = sm.meta[a];
     Sim<P> S;
-    uint32_t st = start_playout<P, JOK, CONS>(S, s, code, meta, kp);
-    for (uint32_t k = 0; st != FINISH; ++k) st = step_playout<P, JOK, CONS>(S, st, k, s, code, kp);
-    const uint32_t win = winner_seat(S);
-    atomicAdd(&sm.hist[a * P + win], 1u);
-    if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)win;
+    uint32_t st = start_playout<P, JOK, CONS, PATH>(S, s, code, meta, kp);
+    for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
+      st = step_playout<P, JOK, CONS, PATH>(S, st, k, s, code, sm.meta, sm.path, a, kp);
+    record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
-  flush_hist(sm.hist, kp.A * P, kp.hist);
+  flush_hist(sm.hist, kp, P);
 }
 
 // ---- refill kernel -------------------------------------------------------
@@ -118,7 +152,7 @@ struct RingView {
     base[(P + 0) * kRing + i] = S.V;
     base[(P + 1) * kRing + i] = S.Q;
     base[(P + 2) * kRing + i] = S.ji;
-    base[(P + 3) * kRing + i] = S.g | (S.pend << 2) | (S.corr << 8) | (st << 16);
+    base[(P + 3) * kRing + i] = S.g | (S.pend << 2) | (S.corr << 8) | (st << 16) | (S.fi << 20);
     base[(P + 4) * kRing + i] = a;
     base[(P + 5) * kRing + i] = s;
     base[(P + 6) * kRing + i] = code;
@@ -134,20 +168,21 @@ struct RingView {
     S.g = pk & 3u;
     S.pend = (pk >> 2) & 31u;
     S.corr = (pk >> 8) & 0xFFu;
-    st = pk >> 16;
+    st = (pk >> 16) & 0xFu;
+    S.fi = pk >> 20;
     a = base[(P + 4) * kRing + i];
     s = base[(P + 5) * kRing + i];
     code = base[(P + 6) * kRing + i];
   }
 };
 
-template <int P, bool JOK, bool CONS>
+template <int P, bool JOK, bool CONS, bool PATH>
 __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_constant__ KParams kp) {
   const Smem sm = setup_smem(kp, P);
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{sh_all + kp.A * (P + 2) + (threadIdx.x >> 5) * RingView<P>::kFields * kRing};
+  const RingView<P> ring{sh_all + kp.A * (P + 3) + kMaxPath + (threadIdx.x >> 5) * RingView<P>::kFields * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
   // slices of ONE action, so no per-lane division).
   uint32_t ca = 0, cs = 0, ce = 0, ccode = 0, cmeta = 0;
@@ -194,11 +229,9 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       Sim<P> T;
       uint32_t pst = FINISH;
       if (valid) {
-        pst = start_playout<P, JOK, CONS>(T, ps, pcode, pmeta, kp);
+        pst = start_playout<P, JOK, CONS, PATH>(T, ps, pcode, pmeta, kp);
         if (pst == FINISH) {                    // decided by the root action alone
-          const uint32_t win = winner_seat(T);
-          atomicAdd(&sm.hist[pa * P + win], 1u);
-          if (kp.winners) kp.winners[(size_t)pa * kp.trace_stride + (ps - kp.trace_s0)] = (uint8_t)win;
+          record(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
           valid = false;
         }
       }
@@ -227,17 +260,15 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
     }
     // ---- one decision step for every running lane
     if (active) {
-      st = step_playout<P, JOK, CONS>(S, st, k, s, code, kp);
+      st = step_playout<P, JOK, CONS, PATH>(S, st, k, s, code, sm.meta, sm.path, a, kp);
       ++k;
-      if (st == FINISH) {
-        const uint32_t win = winner_seat(S);
-        atomicAdd(&sm.hist[a * P + win], 1u);
-        if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)win;
+      if (st == FINISH || st == VOID) {
+        record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
         active = false;
       }
     }
   }
-  flush_hist(sm.hist, kp.A * P, kp.hist);
+  flush_hist(sm.hist, kp, P);
 }
 
 __global__ void det_table_kernel(const uint8_t *__restrict__ plan, uint64_t N, uint4 *__restrict__ out) {
@@ -259,15 +290,17 @@ cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaSt
 typedef void (*KernelFn)(const KParams);
 
 template <int P, bool JOK, bool CONS>
-KernelFn pick_kernel(int variant) {
-  return variant == 1 ? rollout_naive_kernel<P, JOK, CONS> : rollout_refill_kernel<P, JOK, CONS>;
+KernelFn pick_kernel(int variant, bool path) {
+  if (path)
+    return variant == 1 ? rollout_naive_kernel<P, JOK, CONS, true> : rollout_refill_kernel<P, JOK, CONS, true>;
+  return variant == 1 ? rollout_naive_kernel<P, JOK, CONS, false> : rollout_refill_kernel<P, JOK, CONS, false>;
 }
 
-KernelFn select_kernel(int P, bool jok, bool cons, int variant) {
-#define DVC_CASE(PP)                                                                     \
-  if (P == PP) {                                                                         \
-    if (jok) return cons ? pick_kernel<PP, true, true>(variant) : pick_kernel<PP, true, false>(variant); \
-    return cons ? pick_kernel<PP, false, true>(variant) : pick_kernel<PP, false, false>(variant);       \
+KernelFn select_kernel(int P, bool jok, bool cons, int variant, bool path) {
+#define DVC_CASE(PP)                                                                                 \
+  if (P == PP) {                                                                                     \
+    if (jok) return cons ? pick_kernel<PP, true, true>(variant, path) : pick_kernel<PP, true, false>(variant, path); \
+    return cons ? pick_kernel<PP, false, true>(variant, path) : pick_kernel<PP, false, false>(variant, path);       \
   }
   DVC_CASE(2)
   DVC_CASE(3)
@@ -276,15 +309,16 @@ KernelFn select_kernel(int P, bool jok, bool cons, int variant) {
   return nullptr;
 }
 
-cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int block, size_t smem, int *blocks_per_sm) {
-  KernelFn f = select_kernel(P, jok, cons, variant);
+cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, bool path, int block, size_t smem,
+                             int *blocks_per_sm) {
+  KernelFn f = select_kernel(P, jok, cons, variant, path);
   if (!f) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void *)f, block, smem);
 }
 
 cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int grid, int block,
                            size_t smem, cudaStream_t stream) {
-  KernelFn f = select_kernel(P, jok, cons, variant);
+  KernelFn f = select_kernel(P, jok, cons, variant, kp.path_len > 0);
   if (!f) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

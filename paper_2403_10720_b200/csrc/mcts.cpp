@@ -14,13 +14,122 @@
 extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table,
                                int32_t cap, int32_t *n_out, uint32_t *best_code);
 
+namespace {
+
+using namespace dvc;
+
+// ---------------------------------------------------------------------------
+// Depth-capped tree over the viewer's own guesses (PAPER:143-170:
+// nodes keyed by a guess (position, number), depth = the sequence of guesses,
+// no expansion beyond a fixed depth).  Opponents' decisions are chance events
+// drawn by the playout policy.  Each expansion evaluates all children of the
+// selected leaf in ONE GPU batch (leaf parallelism); playouts whose forced
+// path is impossible in their determinization are void and not counted.
+struct Node {
+  uint32_t code;
+  int32_t depth, parent;
+  uint64_t visits = 0, wins = 0, tried = 0;
+  bool expanded = false;
+  std::vector<int32_t> children;
+};
+
+double ucb1(uint64_t w, uint64_t v, uint64_t parent, double c) {
+  return (double)w / (double)v + c * std::sqrt(std::log((double)parent) / (double)v);
+}
+
+int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p, std::vector<uint32_t> &root_codes,
+                std::vector<uint64_t> &rv, std::vector<uint64_t> &rw) {
+  if (p->max_depth < 1 || p->max_depth > kMaxPath)
+    return set_error(DVC_E_CONFIG, "max_depth must be 1..8 for the deep tree");
+  const uint64_t n = p->sims_per_child;
+  const int P = st->P;
+  // children of deeper nodes: the root's guesses, plus STOP under consecutive rules
+  std::vector<uint32_t> deep_codes;
+  for (uint32_t c : root_codes) if (c != DVC_STOP) deep_codes.push_back(c);
+  if (st->consecutive) deep_codes.push_back(DVC_STOP);
+  std::vector<Node> T;
+  T.push_back(Node{0u, 0, -1});
+  std::vector<uint64_t> hist, voids;
+  for (int it = 0; it < p->expansions; ++it) {
+    // ---- selection
+    int32_t x = 0;
+    while (T[x].expanded) {
+      int32_t best = -1;
+      double bv = 0.0;
+      for (int32_t c : T[x].children) {
+        const Node &ch = T[c];
+        if (ch.tried > 0 && ch.visits == 0) continue;          // void so far: impossible path
+        const double v = ch.tried == 0 ? INFINITY : ucb1(ch.wins, ch.visits, T[x].visits, p->c);
+        if (best < 0 || v > bv || (v == bv && ch.code < T[best].code)) { best = c; bv = v; }
+      }
+      if (best < 0) break;
+      x = best;
+    }
+    // path of codes root -> x
+    std::vector<uint32_t> path;
+    for (int32_t y = x; y > 0; y = T[y].parent) path.push_back(T[y].code);
+    std::reverse(path.begin(), path.end());
+    std::vector<int32_t> evaluated;   // nodes whose counts this batch updates
+    const bool expand = !T[x].expanded && T[x].depth < p->max_depth && (x == 0 || T[x].visits > 0);
+    std::vector<uint32_t> batch;
+    std::vector<uint32_t> prefix = path;
+    uint32_t node_word;
+    if (expand) {
+      const std::vector<uint32_t> &cand = (x == 0) ? root_codes : deep_codes;
+      for (uint32_t c : cand) {
+        T[x].children.push_back((int32_t)T.size());
+        T.push_back(Node{c, T[x].depth + 1, x});
+        evaluated.push_back((int32_t)T.size() - 1);
+        batch.push_back(c);
+      }
+      T[x].expanded = true;
+      node_word = (uint32_t)x;
+    } else {
+      if (x == 0) break;                                         // nothing left to do
+      prefix.pop_back();
+      evaluated.push_back(x);
+      batch.push_back(T[x].code);
+      node_word = (uint32_t)T[x].parent;
+    }
+    const uint64_t s0 = T[evaluated[0]].tried;
+    if (s0 + n > (1ull << 32)) return set_error(DVC_E_CONFIG, "a node's sim index range would pass 2^32");
+    hist.assign(batch.size() * (size_t)P, 0);
+    voids.assign(batch.size(), 0);
+    int rc = dvc_rollout_path_ex(s, prefix.data(), (int32_t)prefix.size(), batch.data(), (int32_t)batch.size(),
+                                 p->seed, node_word, s0, s0 + n, hist.data(), voids.data(), p->device);
+    if (rc) return rc;
+    // ---- backpropagation
+    uint64_t dv = 0, dw = 0;
+    for (size_t i = 0; i < evaluated.size(); ++i) {
+      Node &e = T[evaluated[i]];
+      e.tried += n;
+      e.visits += n - voids[i];
+      e.wins += hist[i * P + st->viewer];
+      dv += n - voids[i];
+      dw += hist[i * P + st->viewer];
+    }
+    for (int32_t y = T[evaluated[0]].parent; y >= 0; y = T[y].parent) {
+      T[y].visits += dv;
+      T[y].wins += dw;
+    }
+  }
+  rv.assign(root_codes.size(), 0);
+  rw.assign(root_codes.size(), 0);
+  for (int32_t c : T[0].children) {
+    for (size_t a = 0; a < root_codes.size(); ++a)
+      if (root_codes[a] == T[c].code) { rv[a] = T[c].visits; rw[a] = T[c].wins; }
+  }
+  return DVC_OK;
+}
+
+}  // namespace
+
 extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table,
                                int32_t cap, int32_t *n_out, uint32_t *best_code) {
   using namespace dvc;
   if (!s || !p || !n_out) return set_error(DVC_E_CONFIG, "null argument");
   const State *st = reinterpret_cast<const State *>(s);
   if (st->magic != kMagic) return set_error(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
-  if (!p->flat) return set_error(DVC_E_CONFIG, "flat = 0 (depth-capped tree) is not built yet");
   if (p->expansions < 1 || p->sims_per_child < 1 || !(p->c >= 0.0))
     return set_error(DVC_E_CONFIG, "need expansions >= 1, sims_per_child >= 1, c >= 0");
   int32_t A = 0;
@@ -34,7 +143,11 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
   uint64_t N = 0;
   const uint64_t n = p->sims_per_child;
   int it = 0;
-  {
+  if (!p->flat) {
+    int rc = deep_search(s, st, p, codes, visits, wins);
+    if (rc) return rc;
+    it = p->expansions;
+  } else {
     // Expansion of the root: while children are unvisited, UCB1 selects them
     // one per iteration in ascending code order (+inf ties -> smallest code),
     // each with sims [0, n).  Those iterations are independent, so they run

@@ -15,7 +15,8 @@
 namespace dvc {
 
 constexpr int kMaxActions = 768;
-constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2;
+
+constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
 
 struct KParams {
   uint32_t k0, k1;        // Philox key = (lo32(seed), hi32(seed))
@@ -44,6 +45,9 @@ struct KParams {
   unsigned long long *hist;  // [A * P] global counters (added to)
   uint8_t *winners;       // optional per-playout winner trace
   uint32_t *counter;      // refill kernel's work counter (zeroed per launch)
+  unsigned long long *voids;  // [A] voided playouts (deep-tree batches; may be null)
+  uint32_t path_len;      // forced viewer actions F[0..path_len-1] before the batch action
+  uint32_t path_meta[kMaxPath];  // act_meta of F[i] (relative target from the viewer)
   uint32_t codes[kMaxActions];  // action codes (Philox counter word z)
   uint32_t meta[kMaxActions];   // act_meta(d, pos, v); d = 0 -> STOP
 };
@@ -122,6 +126,7 @@ struct Sim {
   uint32_t g;      // absolute seat of the mover
   uint32_t pend;   // key drawn this turn or kNoKey
   uint32_t corr;   // correct guesses this turn
+  uint32_t fi;     // deep-tree batches: forced viewer actions applied so far
 };
 
 template <int P>
@@ -380,9 +385,10 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
     uint64_t w = __ldg(row + lin);                 // option: pool
     if (rho < w) continue;
     rho -= w;
+    bool placed = false;                           // options d = 1..P-1, in order
 #pragma unroll
     for (uint32_t j = 0; j < 3; ++j) {
-      if (j >= n_opp || q[j] >= op.len[j]) continue;
+      if (placed || j >= n_opp || q[j] >= op.len[j]) continue;
       const uint32_t sl = __ldg(slots + op.slot_off[j] + q[j]);
       const int c = sl & 1u, lo = (int)((sl >> 8) & 0xFFu) - 1, hi = (int)((sl >> 16) & 0xFFu);
       if ((int)(u & 1u) != c || (int)u <= lo || (int)u >= hi) continue;
@@ -391,9 +397,10 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
         hand[j] |= 1u << u;
         q[j] += 1;
         lin += op.stride[j];
-        break;
+        placed = true;
+      } else {
+        rho -= w;
       }
-      rho -= w;
     }
   }
   return make_uint4(hand[0], hand[1], hand[2], op.jinfo);
@@ -430,6 +437,52 @@ __device__ __forceinline__ bool root_action(const Sim<P> &S, uint32_t meta, cons
   *t_out = v;
   *correct = ((Hd >> v) & 1u) && line_pos<JOK>(Hd, v, S.ji, kp) == pos;
   return d == 0;
+}
+
+// Key of the tile at 0-based line position pos of hand Hp (pos < popc(Hp)).
+template <bool JOK>
+__device__ __forceinline__ uint32_t tile_at(uint32_t Hp, uint32_t pos, uint32_t ji, const KParams &kp) {
+  const uint32_t Hn = Hp & kp.numm;
+  if (!JOK || !((Hp >> kp.JB) & 3u)) return nth_bit(Hn, pos);
+  uint32_t before = 0;                      // held jokers left of pos
+#pragma unroll
+  for (uint32_t is_w = 0; is_w < 2; ++is_w) {
+    const uint32_t J = kp.JB + is_w;
+    if (!((Hp >> J) & 1u)) continue;
+    const uint32_t lp = line_pos<JOK>(Hp, J, ji, kp);
+    if (lp == pos) return J;
+    before += lp < pos ? 1u : 0u;
+  }
+  return nth_bit(Hn, pos - before);
+}
+
+// A forced viewer action of a deep-tree batch, at a decision
+// where the viewer moves.  Returns true for STOP; *illegal when the action is
+// not legal in this playout's state (the playout is then void).
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ bool forced_decide(const Sim<P> &S, uint32_t meta, const KParams &kp, uint32_t *t_out,
+                                              bool *correct, bool *illegal) {
+  const uint32_t d = meta & 0xFFu;
+  const uint32_t pos = (meta >> 8) & 0xFFu, v = meta >> 16;
+  *t_out = kNoKey;
+  *correct = false;
+  if (d == 0) {                              // STOP: only after a correct guess this turn
+    *illegal = !(CONS && S.corr >= 1u);
+    return true;
+  }
+  const uint32_t Ht = pick<P>(S.H, d);
+  const uint32_t hid = Ht & ~S.V;
+  bool ok = hid != 0u && pos < (uint32_t)__popc(Ht) && ((kp.T >> v) & 1u) && !((S.H[0] >> v) & 1u) &&
+            !((S.V >> v) & 1u);
+  uint32_t t = kNoKey;
+  if (ok) {
+    t = tile_at<JOK>(Ht, pos, S.ji, kp);
+    ok = ((hid >> t) & 1u) && (t & 1u) == (v & 1u);
+  }
+  *illegal = !ok;
+  *t_out = t;
+  *correct = ok && t == v;
+  return false;
 }
 
 }  // namespace dvc

@@ -24,7 +24,7 @@ HIDDEN = 0xFF
 
 # every symbol include/dvc.h declares
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
-           "dvc_rollout_batch_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async", "dvc_mcts_search",
+           "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async", "dvc_mcts_search",
            "dvc_set_option", "dvc_get_option", "dvc_launch_count", "dvc_last_error", "dvc_shutdown"]
 
 
@@ -91,6 +91,8 @@ def lib():
         L.dvc_legal_actions.argtypes = [P(_State), P(U32), I32, P(I32)]
         L.dvc_rollout_batch.argtypes = [P(_State), P(U32), I32, U64, U64, P(U64)]
         L.dvc_rollout_batch_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, P(U64), P(U64), I32]
+        L.dvc_rollout_path_ex.argtypes = [P(_State), P(U32), I32, P(U32), I32, U64, U32, U64, U64, P(U64), P(U64),
+                                          I32]
         L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
@@ -203,6 +205,19 @@ def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-
     _check(lib().dvc_rollout_batch_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                       hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), None, device))
     return hist
+
+
+def rollout_path_ex(state, path, actions, seed, node_id, sim_begin, sim_end, device=-1):
+    """Deep-tree batch (dvc_rollout_path_ex): returns (hist[A, P], voids[A])."""
+    a, ap = _codes(actions)
+    p, pp = _codes(path if len(path) else [0])
+    P = state.players
+    hist = np.zeros((len(a), P), dtype=np.uint64)
+    voids = np.zeros(len(a), dtype=np.uint64)
+    _check(lib().dvc_rollout_path_ex(ctypes.byref(state._s), pp, len(path), ap, len(a), seed, node_id, sim_begin,
+                                     sim_end, hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                     voids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), device))
+    return hist, voids
 
 
 def _stream_ptr(stream):

@@ -47,4 +47,43 @@ def test_search_errors(dvc):
     with pytest.raises(dvc.DvcError):
         dvc.mcts_search(st, 0, 10, 1)
     with pytest.raises(dvc.DvcError):
-        dvc.mcts_search(st, 4, 10, 1, flat=0)
+        dvc.mcts_search(st, 4, 10, 1, flat=0, max_depth=9)
+
+
+PATH_CASES = ["tests/golden/T2c1.json", "fixtures/c2_d2.json", "fixtures/c3_d2.json", "fixtures/x3_d1.json",
+              "fixtures/xstop_d1.json", "fixtures/x4mid_d2.json", "fixtures/xsmall_d3.json", "fixtures/xlate_d2.json",
+              "fixtures/c4_d5.json"]
+
+
+@pytest.mark.parametrize("kernel", [0, 1], ids=["refill", "naive"])
+@pytest.mark.parametrize("path", PATH_CASES, ids=[os.path.basename(p) for p in PATH_CASES])
+def test_path_batches_equal_oracle(dvc, oracle_lib, path, kernel):
+    """dvc_rollout_path_ex (forced viewer actions, void playouts) == oracle."""
+    import numpy as np
+    d = json.load(open(os.path.join(ROOT, path)))
+    st = dvc.encode(d)
+    L = st.legal_actions()
+    STOP = 0xFFFFFFFF
+    cons = d["rules"].get("consecutive", 1)
+    guesses = [c for c in L if c != STOP]
+    paths = [[guesses[0]], [guesses[-1], guesses[0]], [guesses[len(guesses) // 2]] + guesses[:2]]
+    codes = guesses[:6] + ([STOP] if cons else [])
+    n = 300 if d["rules"]["players"] < 4 else 120
+    with dvc.options(kernel=kernel):
+        for pth in paths:
+            h, v = dvc.rollout_path_ex(st, pth, codes, 13, 5, 7, 7 + n)
+            eh, ev = oracle_lib.rollout_path(d, pth, codes, 13, 5, 7, 7 + n)
+            assert h.astype(np.int64).tolist() == eh and v.astype(np.int64).tolist() == ev, pth
+
+
+@pytest.mark.parametrize("path", CASES[:6], ids=[os.path.basename(p) for p in CASES[:6]])
+def test_deep_search_equals_oracle(dvc, oracle_lib, path):
+    from oracle.search import deep_search
+    d = json.load(open(os.path.join(ROOT, path)))
+    P = d["rules"]["players"]
+    exp_n, n = (5, 48) if P == 4 else (8, 128)
+    best_o, stats_o = deep_search(d, exp_n, n, 33, max_depth=3)
+    st = dvc.encode(d)
+    best_g, stats_g = dvc.mcts_search(st, exp_n, n, 33, max_depth=3, flat=0)
+    assert [tuple(map(int, t)) for t in stats_g] == stats_o
+    assert best_g == best_o

@@ -44,3 +44,24 @@ def test_budget_conservation_and_exact_best(oracle_lib):
     best_p = max(exact)
     codes = [c for c, _, _ in stats]
     assert exact[codes.index(best)] == best_p
+
+
+def test_deep_depth1_equals_flat(oracle_lib):
+    """max_depth 1: the root expansion batch + re-simulation of UCB-selected
+    root children is exactly flat UCB1 with A - 1 more iterations."""
+    from oracle.search import deep_search
+    for name in ("fixtures/c2_d2.json", "fixtures/xstop_d1.json", "tests/golden/T2c1.json"):
+        d = json.load(open(os.path.join(ROOT, name)))
+        A = len(oracle_lib.legal(d))
+        assert deep_search(d, 9, 50, 4, max_depth=1) == flat_search(d, A + 8, 50, 4)
+
+
+def test_deep_search_finds_exact_best(oracle_lib):
+    from oracle.search import deep_search
+    d = json.load(open(os.path.join(GOLD, "T2c1.json")))
+    best, stats = deep_search(d, 12, 200, 9, max_depth=3)
+    exact = [Fraction(x) for x in d["expected"]["p_viewer"]]
+    assert exact[[c for c, _, _ in stats].index(best)] == max(exact)
+    d = json.load(open(os.path.join(GOLD, "E1.json")))
+    best, stats = deep_search(d, 4, 100, 3)
+    assert stats[0][1] == stats[0][2] > 0                    # forced win, no voids at depth 1
