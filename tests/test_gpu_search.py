@@ -87,3 +87,16 @@ def test_deep_search_equals_oracle(dvc, oracle_lib, path):
     best_g, stats_g = dvc.mcts_search(st, exp_n, n, 33, max_depth=3, flat=0)
     assert [tuple(map(int, t)) for t in stats_g] == stats_o
     assert best_g == best_o
+
+
+@pytest.mark.parametrize("flat,seed", [(1, 1), (1, 2), (0, 3)])
+def test_selfplay_equals_oracle(dvc, oracle_lib, flat, seed):
+    """C3 shape (2 players, 26 tiles with jokers): a full self-play game with
+    the GPU searches reproduces the oracle's game move for move."""
+    from paper_2403_10720_b200.selfplay import play_game
+    from oracle.selfplay import play_game as oracle_game
+    kw = dict(expansions=6, sims_per_child=64, flat=flat, max_depth=2)
+    g = play_game(seed, **kw)
+    o = oracle_game(seed, **kw)
+    assert g == o
+    assert g["decisions"] >= 2

@@ -7,8 +7,9 @@ accounted for).  Prints one JSON line per config.
 C1: latency of one decision (encode + dvc_rollout_batch: H2D, kernels, D2H),
     all legal actions x 1000 playouts, 8 opening deals.
 C2: kernel throughput at 10^6 playouts per action, 8 mid-game deals.
-C3: dvc_mcts_search per decision (flat UCT, 64 expansions x 1024 sims per
-    child) on the 4 jokers openings: decisions/s and playouts/s.
+C3: full self-play games (2p, 26 tiles with jokers), each decision a
+    dvc_mcts_search (64 expansions x 1024 sims per child; flat and
+    depth-capped): decisions/s.
 C4: 4 players, 26 tiles, 3 each: ceil(1e8 / A) playouts per action (~1e8 per
     move) on one GPU, 8 deals: playouts/s (the 8-GPU run is bench.py's job).
 """
@@ -78,22 +79,23 @@ def main():
         print(json.dumps({"config": "C2", "desc": "2p/24 tiles/mid-game, all legal x 1e6", "per_deal": rows,
                           "playouts_per_s_mean": sum(r["playouts_per_s"] for r in rows) / len(rows)}), flush=True)
     if "c3" in todo:
-        rows = []
-        for i, d in enumerate(load("c3_d*.json")):
-            st = dvc.encode(d)
-            dvc.mcts_search(st, 4, 1024, 5)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            best, stats = dvc.mcts_search(st, 64, 1024, 1 + i)
-            t = time.perf_counter() - t0
-            assert sum(v for _, v, _ in stats) == 64 * 1024
-            rows.append({"deal": i + 1, "actions": len(stats), "ms_per_decision": round(1e3 * t, 3),
-                         "best": best})
-        print(json.dumps({"config": "C3", "desc": "2p/26 tiles (jokers), flat UCT 64 x 1024 per decision",
-                          "per_deal": rows,
-                          "decisions_per_s": len(rows) / sum(r["ms_per_decision"] / 1e3 for r in rows),
-                          "playouts_per_s": 64 * 1024 * len(rows) / sum(r["ms_per_decision"] / 1e3 for r in rows)}),
-              flush=True)
+        # full self-play games (2p, 26 tiles with jokers), every decision a
+        # dvc_mcts_search of 64 expansions x 1024 playouts per child
+        from paper_2403_10720_b200.selfplay import play_game
+        for flat, label in ((1, "flat UCT (root-parallel, PAPER:180)"), (0, "depth-capped tree, max_depth 4")):
+            rows = []
+            dvc.mcts_search(dvc.encode(load("c3_d*.json")[0]), 4, 1024, 5, flat=flat)
+            for g in range(4):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = play_game(100 + g, expansions=64, sims_per_child=1024, flat=flat, max_depth=4)
+                t = time.perf_counter() - t0
+                rows.append({"game": 100 + g, "decisions": res["decisions"], "winner": res["winner"],
+                             "s": round(t, 3), "ms_per_decision": round(1e3 * t / res["decisions"], 3)})
+            dec = sum(r["decisions"] for r in rows)
+            tt = sum(r["s"] for r in rows)
+            print(json.dumps({"config": "C3", "desc": "2p/26 tiles (jokers) self-play games, %s, 64 x 1024 per "
+                              "decision" % label, "games": rows, "decisions_per_s": dec / tt}), flush=True)
     if "c4" in todo:
         rows = []
         for i, d in enumerate(load("c4_d*.json")):
