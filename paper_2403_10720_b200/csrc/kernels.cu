@@ -184,10 +184,14 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
   const uint32_t lt_mask = (1u << lane) - 1u;
   const RingView<P> ring{sh_all + kp.A * (P + 3) + kMaxPath + (threadIdx.x >> 5) * RingView<P>::kFields * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
-  // slices of ONE action, so no per-lane division).
+  // slices of ONE action, so no per-lane division).  The next batch index is
+  // claimed one batch ahead (lane 0's atomicAdd result is only read at the
+  // next produce), so the atomic's latency is hidden.
   uint32_t ca = 0, cs = 0, ce = 0, ccode = 0, cmeta = 0;
   bool drained = false;
   const uint32_t n_batches = kp.A * kp.nb;
+  uint32_t pref = 0;
+  if (lane == 0) pref = atomicAdd(kp.counter, 1u);
   uint32_t head = 0, count = 0;       // ring (warp-uniform)
   bool active = false;
   uint32_t a = 0, s = 0, code = 0, st = FINISH, k = 0;
@@ -199,10 +203,9 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       uint32_t na = 0, ns = 0, ne = 0, ncode = 0, nmeta = 0;
       bool got = false;
       if (rem < 32u && !drained) {
-        uint32_t b = 0;
-        if (lane == 0) b = atomicAdd(kp.counter, 1u);
-        b = __shfl_sync(0xFFFFFFFFu, b, 0);
+        const uint32_t b = __shfl_sync(0xFFFFFFFFu, pref, 0);
         if (b < n_batches) {
+          if (lane == 0) pref = atomicAdd(kp.counter, 1u);     // claim the following batch
           na = b / kp.nb;
           ns = (b - na * kp.nb) * kBatch;       // relative to s0 (no u32 overflow at 2^32)
           ne = min(ns + kBatch, kp.n_per);
@@ -240,24 +243,6 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       count += __popc(m);
       __syncwarp();
     }
-    // ---- idle lanes pop started playouts
-    const uint32_t need = __ballot_sync(0xFFFFFFFFu, !active);
-    if (need && count) {
-      const uint32_t take = min((uint32_t)__popc(need), count);
-      const uint32_t rank = __popc(need & lt_mask);
-      if (!active && rank < take) {
-        ring.get((head + rank) & (kRing - 1u), S, st, a, s, code);
-        k = 0;
-        active = true;
-      }
-      head = (head + take) & (kRing - 1u);
-      count -= take;
-      __syncwarp();
-    }
-    if (!__any_sync(0xFFFFFFFFu, active)) {
-      if (count == 0 && drained && cs >= ce) break;
-      continue;
-    }
     // ---- one decision step for every running lane
     if (active) {
       st = step_playout<P, JOK, CONS, PATH>(S, st, k, s, code, sm.meta, sm.path, a, kp);
@@ -266,6 +251,24 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
         record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
         active = false;
       }
+    }
+    // ---- lanes without a playout pop started ones (in the same iteration)
+    const uint32_t need = __ballot_sync(0xFFFFFFFFu, !active);
+    if (need) {
+      const uint32_t take = min((uint32_t)__popc(need), count);
+      if (take) {
+        const uint32_t rank = __popc(need & lt_mask);
+        if (!active && rank < take) {
+          ring.get((head + rank) & (kRing - 1u), S, st, a, s, code);
+          k = 0;
+          active = true;
+        }
+        head = (head + take) & (kRing - 1u);
+        count -= take;
+        __syncwarp();
+      }
+      if (take == (uint32_t)__popc(need)) continue;        // every lane busy again
+      if (count == 0 && drained && cs >= ce && !__any_sync(0xFFFFFFFFu, active)) break;
     }
   }
   flush_hist(sm.hist, kp, P);
