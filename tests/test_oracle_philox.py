@@ -3,6 +3,7 @@ known-answer vectors (Random123 kat_vectors, Salmon et al. SC'11), the closed
 form of `choose`'s buckets, rank64 boundaries, and the two oracle-side
 implementations (Python, C++) against each other."""
 
+import os
 import random
 
 import pytest
@@ -77,3 +78,25 @@ def test_counter_layout():
     key = px.seed_key(seed)
     assert px.det_block(seed, node, code, s) == px.philox4x32_10((0xFFFFFFFF, s, code, node), key)
     assert px.step_block(seed, node, code, s, 5) == px.philox4x32_10((5, s, code, node), key)
+
+
+def test_oracle_philox_equals_curand(oracle_lib, tmp_path):
+    """The oracle's Philox4x32-10 equals cuRAND's curand_Philox4x32_10 (a
+    library implementation, compiled host-side from the CUDA toolkit header)
+    on 20000 random (counter, key) pairs."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc) and not shutil.which("nvcc"):
+        pytest.skip("nvcc not available")
+    exe = str(tmp_path / "curand_ref")
+    src = os.path.join(os.path.dirname(__file__), "native", "curand_philox_ref.cu")
+    subprocess.check_call([nvcc, "-O1", "-o", exe, src])
+    rng = random.Random(77)
+    pairs = [tuple(rng.getrandbits(32) for _ in range(6)) for _ in range(20000)]
+    out = subprocess.run([exe], input="\n".join(" ".join(map(str, p)) for p in pairs) + "\n",
+                         capture_output=True, text=True, check=True).stdout.split("\n")
+    for p, line in zip(pairs, out):
+        ref = tuple(int(x) for x in line.split())
+        assert px.philox4x32_10(p[:4], p[4:]) == ref
+        assert oracle_lib.philox_block(p[:4], p[4:]) == ref
