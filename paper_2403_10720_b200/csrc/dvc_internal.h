@@ -25,8 +25,10 @@ constexpr uint8_t kHiddenSlot = 0x80u;    // line[][] entry flag: hidden, low bi
 constexpr int kMaxOpts = 256;             // joint joker options (<= 14*14 in practice)
 constexpr int kMaxPath = 8;               // deep-tree batches: forced viewer actions before the batch action
 
-// jinfo word: jslot(JB) in bits [0,5), jslot(JW) in [5,10), bit 10 = JW precedes
-// JB when both sit in one line (only read when their jslots are equal).
+// Host jinfo word (plan options): jslot(JB) in bits [0,5), jslot(JW) in [5,10),
+// bit 10 = JW precedes JB when both sit in one line (only read when their
+// jslots are equal).  The device converts jslots to threshold keys when it
+// unranks a determinization (rollout.cuh: kap_b / kap_w).
 __host__ __device__ inline uint32_t jslot_b(uint32_t ji) { return ji & 31u; }
 __host__ __device__ inline uint32_t jslot_w(uint32_t ji) { return (ji >> 5) & 31u; }
 
@@ -62,6 +64,9 @@ struct DetOpt {            // one joint joker option (o_JB major, o_JW minor)
 
 struct DetPlanHdr {
   uint32_t n_opts, m, n_opp, bytes;
+  uint32_t viewer_hand;    // the viewer's tiles (jokers' thresholds need the holder's hand)
+  uint32_t jb;             // 2R when jokers are on, else 0
+  uint32_t _pad2[2];
   uint32_t ukeys[28];      // numbered keys of U ascending
   uint32_t opp_known[4];   // keys revealed in opponent d's line (d = 1..3 at [d-1])
   uint32_t opts_off, slots_off, tab_off, _pad;  // byte offsets in the image

@@ -250,6 +250,8 @@ uint64_t build_plan(const State &s, std::vector<uint8_t> *img) {
   DetPlanHdr hdr;
   std::memset(&hdr, 0, sizeof(hdr));
   hdr.n_opp = (uint32_t)(P - 1);
+  hdr.viewer_hand = s.known[s.viewer];
+  hdr.jb = s.jokers ? (uint32_t)JB : 0u;
   for (uint32_t u = s.U & numm; u; u &= u - 1) hdr.ukeys[hdr.m++] = (uint32_t)__builtin_ctz(u);
   for (int d = 1; d < P; ++d) hdr.opp_known[d - 1] = s.known[(s.viewer + d) % P];
   const int m = (int)hdr.m;

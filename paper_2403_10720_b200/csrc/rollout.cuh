@@ -148,11 +148,19 @@ __device__ __forceinline__ uint32_t winner_seat(const Sim<P> &S) {
   return w >= (uint32_t)P ? w - P : w;
 }
 
+// Joker positions on the device are kept as THRESHOLD keys: kappa(J) = the
+// smallest numbered key of J's holder that lies to the right of J (31 when J
+// is right of every numbered tile), plus bit 10 = "JW precedes JB" when both sit
+// in one gap.  J precedes the numbered tile with key v iff kappa(J) <= v, so
+// every joker test is a compare (no select); DESIGN.md §K.
+__device__ __forceinline__ uint32_t kap_b(uint32_t ji) { return ji & 31u; }
+__device__ __forceinline__ uint32_t kap_w(uint32_t ji) { return (ji >> 5) & 31u; }
+
 // Does the joker `other` (held in the same line) come before joker J?
-__device__ __forceinline__ bool joker_first(uint32_t ji, uint32_t other_is_w, uint32_t s_other,
-                                            uint32_t s_j) {
+__device__ __forceinline__ bool joker_first(uint32_t ji, uint32_t other_is_w, uint32_t k_other,
+                                            uint32_t k_j) {
   const bool wfirst = (ji >> 10) & 1u;
-  return s_other < s_j || (s_other == s_j && (other_is_w ? wfirst : !wfirst));
+  return k_other < k_j || (k_other == k_j && (other_is_w ? wfirst : !wfirst));
 }
 
 // Leftmost hidden tile of hand Hp (DESIGN.md §R5 APPLY).
@@ -165,32 +173,31 @@ __device__ __forceinline__ uint32_t leftmost_hidden(uint32_t Hp, uint32_t V, uin
   if (!JOK) return kmin;
   const uint32_t hj = (hid >> kp.JB) & 3u;
   if (!hj) return kmin;
-  // a joker with jslot s precedes the numbered tile of numbered-index r iff s <= r
-  const uint32_t r = hn ? (uint32_t)__popc(Hp & kp.numm & below(kmin)) : 32u;
-  const uint32_t sb = jslot_b(ji), sw = jslot_w(ji);
-  const bool cb = (hj & 1u) && sb <= r;
-  const bool cw = (hj & 2u) && sw <= r;
-  if (cb && cw) return joker_first(ji, 1u, sw, sb) ? kp.JB + 1 : kp.JB;
+  // a hidden joker precedes the lowest hidden numbered tile iff kappa <= its key
+  const uint32_t lim = hn ? kmin : 32u;
+  const uint32_t kb = kap_b(ji), kw = kap_w(ji);
+  const bool cb = (hj & 1u) && kb <= lim;
+  const bool cw = (hj & 2u) && kw <= lim;
+  if (cb && cw) return joker_first(ji, 1u, kw, kb) ? kp.JB + 1 : kp.JB;
   return cb ? kp.JB : (cw ? kp.JB + 1 : kmin);
 }
 
 // 0-based line position of key v held in hand Hp (root action, §R1 "position").
 template <bool JOK>
 __device__ __forceinline__ uint32_t line_pos(uint32_t Hp, uint32_t v, uint32_t ji, const KParams &kp) {
-  const uint32_t sb = jslot_b(ji), sw = jslot_w(ji);
+  const uint32_t kb = kap_b(ji), kw = kap_w(ji);
   if (!JOK || v < kp.JB) {
-    const uint32_t r = __popc(Hp & kp.numm & below(v));
-    uint32_t pos = r;
+    uint32_t pos = __popc(Hp & kp.numm & below(v));
     if (JOK) {
-      pos += ((Hp >> kp.JB) & 1u) && sb <= r;
-      pos += ((Hp >> (kp.JB + 1)) & 1u) && sw <= r;
+      pos += ((Hp >> kp.JB) & 1u) && kb <= v;
+      pos += ((Hp >> (kp.JB + 1)) & 1u) && kw <= v;
     }
     return pos;
   }
   const uint32_t is_w = v - kp.JB;            // 0 = JB, 1 = JW
-  const uint32_t s = is_w ? sw : sb, so = is_w ? sb : sw;
+  const uint32_t k = is_w ? kw : kb, ko = is_w ? kb : kw;
   const bool has_other = (Hp >> (kp.JB + (is_w ^ 1u))) & 1u;
-  return s + ((has_other && joker_first(ji, is_w ^ 1u, so, s)) ? 1u : 0u);
+  return __popc(Hp & kp.numm & below(k)) + ((has_other && joker_first(ji, is_w ^ 1u, ko, k)) ? 1u : 0u);
 }
 
 // Turn start (DESIGN.md §R5 END_TURN): the next alive player after g becomes
@@ -226,29 +233,32 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t wx, uint
   const bool dr = et && S.Q != 0;
   const uint32_t H0 = S.H[0];
   if (JOK) {
-    uint32_t sb = jslot_b(S.ji), sw = jslot_w(S.ji), wf = (S.ji >> 10) & 1u;
+    uint32_t kb = kap_b(S.ji), kw = kap_w(S.ji), wf = (S.ji >> 10) & 1u;
     const bool hasB = (H0 >> kp.JB) & 1u, hasW = (H0 >> (kp.JB + 1)) & 1u;
+    const uint32_t Hn = H0 & kp.numm;
     if (dr && t >= kp.JB) {
       // drawn joker: uniform gap in [0, len]; relative order with the other joker
       const uint32_t gam = choose((uint32_t)__popc(H0) + 1u, wy);
       const uint32_t is_w = t - kp.JB;
       const bool has_other = is_w ? hasB : hasW;
-      const uint32_t lam = is_w ? sb : sw;
-      uint32_t sj = gam;
+      uint32_t sj = gam;                          // numbered tiles left of the new joker
       if (has_other) {
+        const uint32_t lam = __popc(Hn & below(is_w ? kb : kw));   // the other joker's line index
         const bool precedes = gam <= lam;
         sj = precedes ? gam : gam - 1u;
         wf = (is_w ? precedes : !precedes) ? 1u : 0u;
       }
-      if (is_w) sw = sj; else sb = sj;
+      const uint32_t kj = sj < (uint32_t)__popc(Hn) ? nth_bit(Hn, sj) : 31u;
+      if (is_w) kw = kj; else kb = kj;
     } else {
-      // numbered: goes before the first larger numbered tile, so the mover's
-      // jokers with jslot > i shift right
-      const uint32_t i = __popc(H0 & kp.numm & below(t));
-      sb += (dr && hasB && sb > i) ? 1u : 0u;
-      sw += (dr && hasW && sw > i) ? 1u : 0u;
+      // numbered t goes before the first larger numbered tile, i.e. right of
+      // a joker of its gap: it becomes that joker's threshold when no held
+      // numbered key lies in [t, kappa)
+      const uint32_t above = ~below(t);
+      kb = (dr && hasB && t < kb && !(Hn & below(kb) & above)) ? t : kb;
+      kw = (dr && hasW && t < kw && !(Hn & below(kw) & above)) ? t : kw;
     }
-    S.ji = sb | (sw << 5) | (wf << 10);
+    S.ji = kb | (kw << 5) | (wf << 10);
   }
   S.Q = dr ? (S.Q & ~(1u << t)) : S.Q;
   S.H[0] = dr ? (H0 | (1u << t)) : H0;
@@ -281,21 +291,20 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
   uint32_t xs = x;
   if (JOK && ((hid >> kp.JB) & 3u)) {
     // hidden joker(s) in this line: place them first (rare path)
-    const uint32_t Hn = Hd & kp.numm, cntn = __popc(Hn);
     const uint32_t hb = hid & kp.numm & kEven, hw = hid & kp.numm & kOdd;
-    const uint32_t sb = jslot_b(ji), sw = jslot_w(ji);
+    const uint32_t kb = kap_b(ji), kw = kap_w(ji);
     const bool hidB = (hid >> kp.JB) & 1u, hidW = (hid >> (kp.JB + 1)) & 1u;
     uint32_t sel = kNoKey, vidx = 0, sub = 0;
 #pragma unroll
     for (uint32_t is_w = 0; is_w < 2; ++is_w) {
       const bool hidJ = is_w ? hidW : hidB;
       if (!hidJ) continue;
-      const uint32_t s = is_w ? sw : sb;
-      const uint32_t pre = s < cntn ? below(nth_bit(Hn, s)) : kp.numm;
+      const uint32_t kj = is_w ? kw : kb;
+      const uint32_t pre = below(kj);             // numbered keys left of the joker
       uint32_t c = nB * __popc(hb & pre) + nW * __popc(hw & pre);
       const bool hidO = is_w ? hidB : hidW;
-      const uint32_t so = is_w ? sb : sw;
-      if (hidO && joker_first(ji, is_w ^ 1u, so, s)) c += is_w ? nB : nW;
+      const uint32_t ko = is_w ? kb : kw;
+      if (hidO && joker_first(ji, is_w ^ 1u, ko, kj)) c += is_w ? nB : nW;
       const uint32_t nJ = is_w ? nW : nB;
       if (x >= c && x < c + nJ) { sel = kp.JB + is_w; vidx = x - c; }
       else if (x >= c + nJ) sub += nJ;
@@ -403,7 +412,22 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
       }
     }
   }
-  return make_uint4(hand[0], hand[1], hand[2], op.jinfo);
+  // joker slots -> threshold keys (the k-th numbered key of the holder, or 31)
+  uint32_t ji = op.jinfo & (1u << 10);
+  if (hdr->jb) {
+#pragma unroll
+    for (uint32_t is_w = 0; is_w < 2; ++is_w) {
+      const uint32_t J = hdr->jb + is_w;
+      uint32_t H = (hdr->viewer_hand >> J) & 1u ? hdr->viewer_hand : 0u;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) H = ((hand[j] >> J) & 1u) ? hand[j] : H;
+      const uint32_t Hn = H & below(hdr->jb);
+      const uint32_t sj = (op.jinfo >> (5 * is_w)) & 31u;
+      const uint32_t kj = (H && sj < (uint32_t)__popc(Hn)) ? nth_bit(Hn, sj) : 31u;
+      ji |= kj << (5 * is_w);
+    }
+  }
+  return make_uint4(hand[0], hand[1], hand[2], ji);
 }
 
 // Determinization (a2): state of playout with determinization block D.
