@@ -193,6 +193,15 @@ typedef struct { uint32_t code, _pad; uint64_t visits, wins; } dvc_action_stat;
 int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table, int32_t cap,
                     int32_t *n_out, uint32_t *best_code);
 
+/* Debug build only (libdvc_debug.so, compiled with -DDVC_DEBUG): out3 =
+ * {invariant violations, code of the first one, finished playouts checked}
+ * accumulated on `device` since its scratch was created (codes: 1 hands/pool
+ * not disjoint, 2 tiles not conserved, 3 a pool tile revealed, 4 bad joker
+ * threshold, 5 mover dead, 6 too many decisions, 7 not exactly one reveal per
+ * guess, 8 STOP without a correct guess, 9 not exactly one survivor).  The
+ * release library returns DVC_E_CONFIG. */
+int dvc_debug_counters(int32_t device, uint32_t *out3);
+
 /* Number of kernel launches the library enqueued since the last reset
  * (reset = 1 zeroes it); lets callers count GPU launches in a timed region. */
 uint64_t dvc_launch_count(int32_t reset);

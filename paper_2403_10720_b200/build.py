@@ -22,29 +22,37 @@ def _nvcc():
             return c
 
 
-def _stale():
-    if not os.path.exists(LIB):
+def _stale(lib=LIB):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "dvc.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + ".tmp.%d" % os.getpid()
+LIB_DEBUG = os.path.join(HERE, "libdvc_debug.so")
+
+
+def build(force=False, verbose=False, debug=False):
+    """Release libdvc.so, or (debug=True) libdvc_debug.so with the device-side
+    invariant checks (-DDVC_DEBUG; dvc_debug_counters)."""
+    out = LIB_DEBUG if debug else LIB
+    if not force and not _stale(out):
+        return out
+    tmp = out + ".tmp.%d" % os.getpid()
     cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-O2", "-I", os.path.join(HERE, "..", "include"), "-o", tmp]
+    if debug:
+        cmd += ["-DDVC_DEBUG"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     cmd += [os.path.join(CSRC, f) for f in SOURCES]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    print(build(force=True, verbose="--verbose" in sys.argv, debug="--debug" in sys.argv))

@@ -54,6 +54,7 @@ struct DeviceScratch {
   uint32_t *d_counters = nullptr;
   uint32_t next_counter = 0;
   unsigned long long *d_hist = nullptr;  // blocking calls
+  uint32_t *d_debug = nullptr;           // DVC_DEBUG builds: invariant counters
   size_t hist_cap = 0;
   cudaStream_t stream = nullptr;         // blocking calls
   std::list<PlanEntry> plans;            // LRU, front = most recent
@@ -86,6 +87,11 @@ int get_scratch(int device, DeviceScratch **out) {
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaDeviceGetAttribute"); }
   e = cudaMalloc(&d->d_counters, kCounterSlots * sizeof(uint32_t));
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaMalloc(counters)"); }
+#ifdef DVC_DEBUG
+  e = cudaMalloc(&d->d_debug, 4 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(d->d_debug, 0, 4 * sizeof(uint32_t));
+  if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaMalloc(debug)"); }
+#endif
   e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) { cudaFree(d->d_counters); delete d; return cuda_fail(e, "cudaStreamCreate"); }
   g_dev[device] = d;
@@ -220,6 +226,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   kp.pend0 = st->pend_key >= 0 ? (uint32_t)st->pend_key : kNoKey;
   kp.corr0 = (uint32_t)st->corr;
   kp.N = st->N;
+  kp.debug = d->d_debug;
   kp.table = plan->d_table;
   kp.plan = plan->d_plan;
   kp.hist = d_hist;
@@ -503,6 +510,23 @@ int dvc_get_option(const char *name, int64_t *value) {
   else if (n == "chunk") *value = g_chunk;
   else return set_err(DVC_E_CONFIG, "unknown option " + n);
   return DVC_OK;
+}
+
+int dvc_debug_counters(int32_t device, uint32_t *out3) {
+#ifdef DVC_DEBUG
+  if (!out3) return set_err(DVC_E_CONFIG, "null argument");
+  std::lock_guard<std::mutex> lock(g_mu);
+  DeviceScratch *d = nullptr;
+  int rc = get_scratch(device, &d);
+  if (rc) return rc;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(out3, d->d_debug, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "debug counters");
+  return DVC_OK;
+#else
+  (void)device; (void)out3;
+  return set_err(DVC_E_CONFIG, "not a DVC_DEBUG build (libdvc_debug.so has the invariant checks)");
+#endif
 }
 
 uint64_t dvc_launch_count(int32_t reset) {

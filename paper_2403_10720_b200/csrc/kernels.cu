@@ -95,6 +95,12 @@ __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_
                                                  const KParams &kp) {
   const uint4 B = philox_rk(k, s, code, kp.node, kp);
   turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
+#ifdef DVC_DEBUG
+  dbg_check_state<P, JOK>(S, kp);
+  if (!(S.H[0] & ~S.V)) dbg_fail(kp, 5);                       // the mover is alive
+  if (k >= 2u * (uint32_t)__popc(kp.T)) dbg_fail(kp, 6);        // decisions <= 2(|T|-1)
+  const uint32_t v_before = __popc(S.V);
+#endif
   uint32_t t;
   bool correct;
   bool stop;
@@ -109,7 +115,22 @@ __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_
   } else {
     stop = decide<P, JOK, CONS>(S, B.z, kp, &t, &correct);
   }
+#ifdef DVC_DEBUG
+  const uint32_t r = stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
+  if ((uint32_t)__popc(S.V) != v_before + (stop ? 0u : 1u)) dbg_fail(kp, 7);   // one reveal per guess
+  if (stop && !(CONS && S.corr >= 1u)) dbg_fail(kp, 8);                        // STOP only after a correct guess
+  if (r == FINISH) {
+    uint32_t alive = 0;
+#pragma unroll
+    for (int d = 0; d < P; ++d) alive += (S.H[d] & ~S.V) ? 1u : 0u;
+    if (alive != 1u) dbg_fail(kp, 9);                                         // one survivor
+    atomicAdd(&kp.debug[2], 1u);
+  }
+  dbg_check_state<P, JOK>(S, kp);
+  return r;
+#else
   return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
+#endif
 }
 
 template <int P, bool JOK, bool CONS, bool PATH>

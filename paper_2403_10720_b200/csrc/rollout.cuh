@@ -46,6 +46,7 @@ struct KParams {
   uint8_t *winners;       // optional per-playout winner trace
   uint32_t *counter;      // refill kernel's work counter (zeroed per launch)
   unsigned long long *voids;  // [A] voided playouts (deep-tree batches; may be null)
+  uint32_t *debug;        // DVC_DEBUG builds: [violations, first violation code, playouts checked]
   uint32_t path_len;      // forced viewer actions F[0..path_len-1] before the batch action
   uint32_t path_meta[kMaxPath];  // act_meta of F[i] (relative target from the viewer)
   uint32_t codes[kMaxActions];  // action codes (Philox counter word z)
@@ -462,6 +463,37 @@ __device__ __forceinline__ bool root_action(const Sim<P> &S, uint32_t meta, cons
   *correct = ((Hd >> v) & 1u) && line_pos<JOK>(Hd, v, S.ji, kp) == pos;
   return d == 0;
 }
+
+#ifdef DVC_DEBUG
+// ---- invariant checks of the debug build (SURVEY §8(c.8) "Rules" row): tile
+// conservation, revealed tiles held by someone, joker thresholds valid, the
+// mover alive with >= 1 legal decision, exactly one reveal per guess, one
+// survivor at the end, decisions bounded by 2(|T|-1).
+__device__ __forceinline__ void dbg_fail(const KParams &kp, uint32_t code) {
+  atomicAdd(&kp.debug[0], 1u);
+  atomicCAS(&kp.debug[1], 0u, code);
+}
+template <int P, bool JOK>
+__device__ __forceinline__ void dbg_check_state(const Sim<P> &S, const KParams &kp) {
+  uint32_t uni = S.Q;
+  bool disjoint = true;
+#pragma unroll
+  for (int d = 0; d < P; ++d) { disjoint = disjoint && !(uni & S.H[d]); uni |= S.H[d]; }
+  if (!disjoint) dbg_fail(kp, 1);
+  if (uni != kp.T) dbg_fail(kp, 2);
+  if (S.V & S.Q) dbg_fail(kp, 3);
+  if (JOK) {
+#pragma unroll
+    for (uint32_t is_w = 0; is_w < 2; ++is_w) {
+      const uint32_t J = kp.JB + is_w, kj = is_w ? kap_w(S.ji) : kap_b(S.ji);
+      uint32_t holder = 0;
+#pragma unroll
+      for (int d = 0; d < P; ++d) holder = ((S.H[d] >> J) & 1u) ? S.H[d] : holder;
+      if (holder && kj != 31u && !((holder & kp.numm) >> kj & 1u)) dbg_fail(kp, 4);
+    }
+  }
+}
+#endif
 
 // Key of the tile at 0-based line position pos of hand Hp (pos < popc(Hp)).
 template <bool JOK>

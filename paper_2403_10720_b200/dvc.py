@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdvc.so")
+# DVC_DEBUG=1 selects the debug build (device-side invariant checks)
+LIB_PATH = os.path.join(HERE, "libdvc_debug.so" if os.environ.get("DVC_DEBUG") == "1" else "libdvc.so")
 
 DVC_OK = 0
 ERRORS = {-1: "DVC_E_CONFIG", -2: "DVC_E_PROTOCOL", -3: "DVC_E_ILLEGAL",
@@ -25,7 +26,8 @@ HIDDEN = 0xFF
 # every symbol include/dvc.h declares
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
            "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async", "dvc_mcts_search",
-           "dvc_set_option", "dvc_get_option", "dvc_launch_count", "dvc_last_error", "dvc_shutdown"]
+           "dvc_set_option", "dvc_get_option", "dvc_debug_counters", "dvc_launch_count", "dvc_last_error",
+           "dvc_shutdown"]
 
 
 class DvcError(RuntimeError):
@@ -96,6 +98,7 @@ def lib():
         L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
+        L.dvc_debug_counters.argtypes = [I32, P(U32)]
         L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
         L.dvc_get_option.argtypes = [ctypes.c_char_p, P(I64)]
         L.dvc_launch_count.argtypes = [I32]
@@ -288,6 +291,13 @@ class options:
     def __exit__(self, *exc):
         for k, v in self.old.items():
             set_option(k, v)
+
+
+def debug_counters(device=-1):
+    """(violations, first code, playouts checked) -- debug build only."""
+    out = (ctypes.c_uint32 * 3)()
+    _check(lib().dvc_debug_counters(device, out))
+    return tuple(out)
 
 
 def launch_count(reset=False):
