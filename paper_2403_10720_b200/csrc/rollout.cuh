@@ -290,27 +290,30 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
                                             uint32_t *t_out, uint32_t *vidx_out) {
   const uint32_t hid = Hd & ~V;
   uint32_t xs = x;
-  if (JOK && ((hid >> kp.JB) & 3u)) {
-    // hidden joker(s) in this line: place them first (rare path)
+  uint32_t sel = kNoKey, vidx_j = 0;
+  if (JOK) {
+    // hidden jokers of this line are placed first, by their thresholds.  Done
+    // branch-free for every lane (in 4-player games nearly every warp-step has
+    // some lane whose target line holds a hidden joker).
     const uint32_t hb = hid & kp.numm & kEven, hw = hid & kp.numm & kOdd;
     const uint32_t kb = kap_b(ji), kw = kap_w(ji);
     const bool hidB = (hid >> kp.JB) & 1u, hidW = (hid >> (kp.JB + 1)) & 1u;
-    uint32_t sel = kNoKey, vidx = 0, sub = 0;
+    uint32_t sub = 0;
 #pragma unroll
     for (uint32_t is_w = 0; is_w < 2; ++is_w) {
       const bool hidJ = is_w ? hidW : hidB;
-      if (!hidJ) continue;
       const uint32_t kj = is_w ? kw : kb;
       const uint32_t pre = below(kj);             // numbered keys left of the joker
       uint32_t c = nB * __popc(hb & pre) + nW * __popc(hw & pre);
       const bool hidO = is_w ? hidB : hidW;
       const uint32_t ko = is_w ? kb : kw;
-      if (hidO && joker_first(ji, is_w ^ 1u, ko, kj)) c += is_w ? nB : nW;
+      c += (hidO && joker_first(ji, is_w ^ 1u, ko, kj)) ? (is_w ? nB : nW) : 0u;
       const uint32_t nJ = is_w ? nW : nB;
-      if (x >= c && x < c + nJ) { sel = kp.JB + is_w; vidx = x - c; }
-      else if (x >= c + nJ) sub += nJ;
+      const bool here = hidJ && x >= c && x < c + nJ;
+      sel = here ? kp.JB + is_w : sel;
+      vidx_j = here ? x - c : vidx_j;
+      sub += (hidJ && x >= c + nJ) ? nJ : 0u;
     }
-    if (sel != kNoKey) { *t_out = sel; *vidx_out = vidx; return; }
     xs = x - sub;
   }
   const uint32_t hB = hid & kp.numm & kEven, hW = hid & kp.numm & kOdd;
@@ -322,8 +325,9 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
     const uint32_t c = nB * __popc(hB & m) + nW * __popc(hW & m);
     if (c <= xs) { k = kk; base = c; }
   }
-  *t_out = k;
-  *vidx_out = xs - base;
+  const bool jok = JOK && sel != kNoKey;
+  *t_out = jok ? sel : k;
+  *vidx_out = jok ? vidx_j : xs - base;
 }
 
 // One random decision (DESIGN.md §R5 loop body after the draw): i =
