@@ -100,14 +100,6 @@ struct Game {
     for (int p = 0; p < rules.P; ++p) if (alive(p)) return p;
     throw std::runtime_error("no winner");
   }
-  bool in_hand(int p, int k) const {
-    for (const Tile &t : lines[p]) if (t.key == k) return true;
-    return false;
-  }
-  bool revealed_anywhere(int k) const {
-    for (const auto &ln : lines) for (const Tile &t : ln) if (t.rev && t.key == k) return true;
-    return false;
-  }
   // A numbered key goes immediately before the first numbered tile with a
   // larger key (right of any joker in its gap).
   void insert_numbered(int p, int k) {

@@ -22,7 +22,6 @@ constexpr uint32_t kEven = 0x55555555u;   // black keys (incl. JB = 2R)
 constexpr uint32_t kOdd = 0xAAAAAAAAu;    // white keys (incl. JW = 2R+1)
 constexpr uint32_t kNoKey = 31u;          // "NONE" for pend
 constexpr uint8_t kHiddenSlot = 0x80u;    // line[][] entry flag: hidden, low bit = colour
-constexpr int kMaxOpts = 256;             // joint joker options (<= 14*14 in practice)
 constexpr int kMaxPath = 8;               // deep-tree batches: forced viewer actions before the batch action
 
 // Host jinfo word (plan options): jslot(JB) in bits [0,5), jslot(JW) in [5,10),
@@ -41,7 +40,6 @@ struct State {
   uint32_t V;          // revealed keys (any line)
   uint32_t U;          // unaccounted keys (not the viewer's, not revealed)
   uint32_t known[4];   // seat -> keys the viewer knows that seat holds
-  uint32_t jinfo_viewer;  // jslots of jokers in the viewer's line (others 0)
   int32_t line_len[4];
   uint8_t line[4][26];    // key, or kHiddenSlot|colour
   uint64_t N;             // |Det(O)|

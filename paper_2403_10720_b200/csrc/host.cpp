@@ -93,19 +93,6 @@ int encode(const dvc_observation *o, State *out, const char **err) {
     }
   }
   s.U = s.T & ~s.known[s.viewer] & ~s.V;
-  // viewer's jokers: jslot = #numbered tiles to their left
-  {
-    int nnum = 0, posB = -1, posW = -1;
-    uint32_t ji = 0;
-    for (int i = 0; i < s.line_len[s.viewer]; ++i) {
-      int k = s.line[s.viewer][i];
-      if (k == 2 * R) { ji |= (uint32_t)nnum; posB = i; }
-      else if (k == 2 * R + 1) { ji |= (uint32_t)nnum << 5; posW = i; }
-      else ++nnum;
-    }
-    if (posB >= 0 && posW >= 0 && posW < posB) ji |= 1u << 10;
-    s.jinfo_viewer = ji;
-  }
   // ---- determinization count
   {
     std::vector<uint8_t> img;

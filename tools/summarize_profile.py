@@ -34,6 +34,10 @@ KEYS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
     "smsp__warps_eligible.avg.per_cycle_active": "eligible_warps",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
+    "smsp__sass_average_branch_targets_threads_uniform.pct": "branch_targets_uniform_pct",
+    "smsp__sass_branch_targets_threads_divergent.sum": "branch_targets_divergent",
+    "smsp__inst_executed_op_branch.sum": "branch_inst",
+    "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active": "pipe_uniform_pct",
 }
 
 
