@@ -142,6 +142,14 @@ CONFIGS = {
     "xc0": (dict(players=2, ranks=12, jokers=0, consecutive=0), 4, 8, 0, False, range(1, 5)),
     "x4mid": (dict(players=4, ranks=12, jokers=1, consecutive=1), 3, 10, 0, False, range(1, 5)),
     "xsmall": (dict(players=3, ranks=4, jokers=1, consecutive=1), 2, 2, 0, False, range(1, 5)),
+    # every kernel instantiation (players x jokers x consecutive) gets fixtures
+    "x3nj": (dict(players=3, ranks=12, jokers=0, consecutive=1), 4, 5, 0, False, range(1, 4)),
+    "x4nj": (dict(players=4, ranks=12, jokers=0, consecutive=0), 3, 6, 0, False, range(1, 4)),
+    "x3c0": (dict(players=3, ranks=12, jokers=1, consecutive=0), 4, 4, 0, False, range(1, 4)),
+    "x2jc0": (dict(players=2, ranks=12, jokers=1, consecutive=0), 4, 6, 0, False, range(1, 4)),
+    "x4njc1": (dict(players=4, ranks=12, jokers=0, consecutive=1), 3, 2, 0, False, range(1, 4)),
+    "x3njc0": (dict(players=3, ranks=12, jokers=0, consecutive=0), 4, 3, 0, False, range(1, 4)),
+    "x4jc0": (dict(players=4, ranks=12, jokers=1, consecutive=0), 3, 3, 0, False, range(1, 4)),
 }
 
 
