@@ -9,6 +9,7 @@
 #include <cstring>
 #include <list>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -48,15 +49,21 @@ struct PlanEntry {
 constexpr int kCounterSlots = 4096;
 constexpr size_t kPlanCacheMax = 16;
 
+// Stream + device histogram used by the BLOCKING entry points of one host
+// thread, so threads (e.g. concurrent self-play games) overlap on the GPU.
+struct HostLane {
+  cudaStream_t stream = nullptr;
+  unsigned long long *d_hist = nullptr;
+  size_t hist_cap = 0;
+};
+
 struct DeviceScratch {
   int device = -1;
   int num_sms = 0;
   uint32_t *d_counters = nullptr;
   uint32_t next_counter = 0;
-  unsigned long long *d_hist = nullptr;  // blocking calls
   uint32_t *d_debug = nullptr;           // DVC_DEBUG builds: invariant counters
-  size_t hist_cap = 0;
-  cudaStream_t stream = nullptr;         // blocking calls
+  std::unordered_map<std::thread::id, HostLane> lanes;
   std::list<PlanEntry> plans;            // LRU, front = most recent
   std::unordered_map<uint64_t, int> occupancy;   // resident blocks per SM per launch shape
 };
@@ -92,10 +99,28 @@ int get_scratch(int device, DeviceScratch **out) {
   if (e == cudaSuccess) e = cudaMemset(d->d_debug, 0, 4 * sizeof(uint32_t));
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaMalloc(debug)"); }
 #endif
-  e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
-  if (e != cudaSuccess) { cudaFree(d->d_counters); delete d; return cuda_fail(e, "cudaStreamCreate"); }
   g_dev[device] = d;
   *out = d;
+  return DVC_OK;
+}
+
+// The calling thread's lane on device d with a histogram of >= n counters
+// (caller holds g_mu).
+int get_lane(DeviceScratch *d, size_t n, HostLane **out) {
+  HostLane &L = d->lanes[std::this_thread::get_id()];
+  if (!L.stream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { L.stream = nullptr; return cuda_fail(e, "cudaStreamCreate"); }
+  }
+  if (L.hist_cap < n) {
+    if (L.d_hist) cudaFree(L.d_hist);
+    L.d_hist = nullptr;
+    L.hist_cap = 0;
+    cudaError_t e = cudaMalloc(&L.d_hist, n * sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(hist)");
+    L.hist_cap = n;
+  }
+  *out = &L;
   return DVC_OK;
 }
 
@@ -348,27 +373,23 @@ int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_
   }
   const size_t n = (size_t)n_actions * st->P;
   DeviceScratch *d = nullptr;
+  HostLane *L = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_mu);
     int rc = get_scratch(device, &d);
     if (rc) return rc;
-    if (d->hist_cap < n) {
-      if (d->d_hist) cudaFree(d->d_hist);
-      d->d_hist = nullptr;
-      cudaError_t e = cudaMalloc(&d->d_hist, n * sizeof(unsigned long long));
-      if (e != cudaSuccess) { d->hist_cap = 0; return cuda_fail(e, "cudaMalloc(hist)"); }
-      d->hist_cap = n;
-    }
-    cudaError_t e = cudaMemsetAsync(d->d_hist, 0, n * sizeof(unsigned long long), d->stream);
+    rc = get_lane(d, n, &L);
+    if (rc) return rc;
+    cudaError_t e = cudaMemsetAsync(L->d_hist, 0, n * sizeof(unsigned long long), L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
   }
-  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d->d_hist, nullptr, d->device,
-                   d->stream, nullptr);
+  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
+                   L->stream, nullptr);
   if (rc) return rc;
   std::vector<unsigned long long> tmp(n);
-  cudaError_t e = cudaMemcpyAsync(tmp.data(), d->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                  d->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+  cudaError_t e = cudaMemcpyAsync(tmp.data(), L->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  L->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rollout");
   for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
   if (visits)
@@ -401,31 +422,27 @@ int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_l
   }
   const size_t n = (size_t)n_actions * st->P;
   DeviceScratch *d = nullptr;
+  HostLane *L = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_mu);
     int rc = get_scratch(device, &d);
     if (rc) return rc;
-    if (d->hist_cap < n + (size_t)n_actions) {
-      if (d->d_hist) cudaFree(d->d_hist);
-      d->d_hist = nullptr;
-      cudaError_t e = cudaMalloc(&d->d_hist, (n + n_actions) * sizeof(unsigned long long));
-      if (e != cudaSuccess) { d->hist_cap = 0; return cuda_fail(e, "cudaMalloc(hist)"); }
-      d->hist_cap = n + n_actions;
-    }
-    cudaError_t e = cudaMemsetAsync(d->d_hist, 0, (n + n_actions) * sizeof(unsigned long long), d->stream);
+    rc = get_lane(d, n + (size_t)n_actions, &L);
+    if (rc) return rc;
+    cudaError_t e = cudaMemsetAsync(L->d_hist, 0, (n + n_actions) * sizeof(unsigned long long), L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
   }
   PathArg pa;
   pa.codes = path;
   pa.len = path_len;
-  pa.d_voids = d->d_hist + n;
-  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d->d_hist, nullptr, d->device,
-                   d->stream, nullptr, pa);
+  pa.d_voids = L->d_hist + n;
+  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
+                   L->stream, nullptr, pa);
   if (rc) return rc;
   std::vector<unsigned long long> tmp(n + n_actions);
-  cudaError_t e = cudaMemcpyAsync(tmp.data(), d->d_hist, tmp.size() * sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, d->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(d->stream);
+  cudaError_t e = cudaMemcpyAsync(tmp.data(), L->d_hist, tmp.size() * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, L->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rollout");
   for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
   if (voids)
@@ -545,8 +562,10 @@ void dvc_shutdown(void) {
     cudaDeviceSynchronize();
     for (auto &p : d->plans) free_plan(p);
     if (d->d_counters) cudaFree(d->d_counters);
-    if (d->d_hist) cudaFree(d->d_hist);
-    if (d->stream) cudaStreamDestroy(d->stream);
+    for (auto &kv2 : d->lanes) {
+      if (kv2.second.d_hist) cudaFree(kv2.second.d_hist);
+      if (kv2.second.stream) cudaStreamDestroy(kv2.second.stream);
+    }
     delete d;
   }
   g_dev.clear();

@@ -143,3 +143,14 @@ def play_game(seed, players=2, ranks=12, jokers=1, consecutive=1, per=4, expansi
         if out == "END_TURN":
             ref.next_turn()
     raise RuntimeError("game did not finish within %d decisions" % max_decisions)
+
+
+def play_games(seeds, threads=8, **kw):
+    """Several self-play games at once, one host thread each: every thread's
+    blocking searches run on its own CUDA stream (the library keeps a stream
+    per host thread), so the small per-decision batches of different games
+    overlap on the GPU.  Results are identical to playing the games one by
+    one (every decision is a pure function of its inputs)."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(lambda s: play_game(s, **kw), seeds))

@@ -100,3 +100,16 @@ def test_selfplay_equals_oracle(dvc, oracle_lib, flat, seed):
     o = oracle_game(seed, **kw)
     assert g == o
     assert g["decisions"] >= 2
+
+
+def test_concurrent_selfplay_equals_sequential(dvc):
+    """Games played on 6 host threads (one CUDA stream each) equal the same
+    games played one at a time."""
+    from paper_2403_10720_b200.selfplay import play_game, play_games
+    kw = dict(expansions=8, sims_per_child=128, flat=1)
+    seeds = [11, 12, 13, 14, 15, 16]
+    seq = [play_game(s, **kw) for s in seeds]
+    assert play_games(seeds, threads=6, **kw) == seq
+    kw = dict(expansions=6, sims_per_child=64, flat=0, max_depth=3)
+    seq = [play_game(s, **kw) for s in seeds[:3]]
+    assert play_games(seeds[:3], threads=3, **kw) == seq

@@ -94,8 +94,17 @@ def main():
                              "s": round(t, 3), "ms_per_decision": round(1e3 * t / res["decisions"], 3)})
             dec = sum(r["decisions"] for r in rows)
             tt = sum(r["s"] for r in rows)
+            # the same kind of games, 16 at a time on 16 host threads / CUDA streams
+            from paper_2403_10720_b200.selfplay import play_games
+            t0 = time.perf_counter()
+            many = play_games(list(range(200, 216)), threads=16, expansions=64, sims_per_child=1024, flat=flat,
+                              max_depth=4)
+            tm = time.perf_counter() - t0
             print(json.dumps({"config": "C3", "desc": "2p/26 tiles (jokers) self-play games, %s, 64 x 1024 per "
-                              "decision" % label, "games": rows, "decisions_per_s": dec / tt}), flush=True)
+                              "decision" % label, "games": rows, "decisions_per_s": dec / tt,
+                              "concurrent_16_games": {"decisions": sum(g["decisions"] for g in many), "s": round(tm, 3),
+                                                      "decisions_per_s": sum(g["decisions"] for g in many) / tm}}),
+                  flush=True)
     if "c4" in todo:
         rows = []
         for i, d in enumerate(load("c4_d*.json")):
