@@ -108,6 +108,15 @@ def test_rollout_without_gpu_fails_loudly(dvc):
     with pytest.raises(dvc.DvcError) as e:
         dvc.rollout_batch(st, codes, 0, 1)
     assert e.value.code == -1
+    with pytest.raises(dvc.DvcError) as e:
+        dvc.rollout_batch(st, [], 10, 1)                     # empty action list
+    assert e.value.code == -1
+    with pytest.raises(dvc.DvcError) as e:
+        dvc.rollout_batch(st, codes * 400, 10, 1)            # more than 768 actions
+    assert e.value.code == -1
+    with pytest.raises(dvc.DvcError) as e:
+        dvc.rollout_batch(st, codes, 1 << 32, 1)             # sim indices are 32-bit
+    assert e.value.code == -1
 
 
 def test_options_roundtrip(dvc):
