@@ -24,12 +24,15 @@ cudaError_t launch_table(const uint8_t *plan, uint64_t N, uint4 *out, cudaStream
 cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaStream_t stream);
 cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, bool path, int block, size_t smem,
                              int *blocks_per_sm);
+cudaError_t search_occupancy(int P, bool jok, bool cons, int block, size_t smem, int *blocks_per_sm);
+cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, int grid,
+                               int block, size_t smem, cudaStream_t stream);
 
 namespace {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_kernel{0}, g_block{128}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1},
-    g_chunk{1ll << 31};
+    g_chunk{1ll << 31}, g_search_device{0};
 std::atomic<uint64_t> g_launches{0};
 
 int set_err(int code, const std::string &msg) {
@@ -55,6 +58,8 @@ struct HostLane {
   cudaStream_t stream = nullptr;
   unsigned long long *d_hist = nullptr;
   size_t hist_cap = 0;
+  unsigned char *d_search = nullptr;     // device flat search: lnN, delta, out, batch_pos
+  size_t search_cap = 0;
 };
 
 struct DeviceScratch {
@@ -189,6 +194,31 @@ const State *as_state(const dvc_state *s) {
   return st->magic == kMagic ? st : nullptr;
 }
 
+// Batch-invariant KParams fields: Philox key + round keys, root state, plan/table.
+void fill_kparams(KParams &kp, const State *st, uint64_t seed, uint32_t node_id, uint32_t n_actions,
+                  const PlanEntry *plan, const DeviceScratch *d) {
+  kp.k0 = (uint32_t)seed; kp.k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    kp.rk[2 * r] = kp.k0 + (uint32_t)r * 0x9E3779B9u;
+    kp.rk[2 * r + 1] = kp.k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  kp.node = node_id;
+  kp.A = n_actions;
+  kp.g0 = (uint32_t)st->viewer;
+  kp.Hv = st->known[st->viewer];
+  kp.V0 = st->V;
+  kp.U = st->U;
+  kp.T = st->T;
+  kp.numm = (1u << (2 * st->R)) - 1u;
+  kp.JB = (uint32_t)(2 * st->R);
+  kp.pend0 = st->pend_key >= 0 ? (uint32_t)st->pend_key : kNoKey;
+  kp.corr0 = (uint32_t)st->corr;
+  kp.N = st->N;
+  kp.debug = d->d_debug;
+  kp.table = plan->d_table;
+  kp.plan = plan->d_plan;
+}
+
 // Core enqueue: adds hist for [sim_begin, sim_end) into d_hist on stream.
 struct PathArg {
   const uint32_t *codes = nullptr;
@@ -234,26 +264,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   if (rc) return rc;
 
   const int P = st->P;
-  kp.k0 = (uint32_t)seed; kp.k1 = (uint32_t)(seed >> 32);
-  for (int r = 0; r < 10; ++r) {
-    kp.rk[2 * r] = kp.k0 + (uint32_t)r * 0x9E3779B9u;
-    kp.rk[2 * r + 1] = kp.k1 + (uint32_t)r * 0xBB67AE85u;
-  }
-  kp.node = node_id;
-  kp.A = (uint32_t)n_actions;
-  kp.g0 = (uint32_t)st->viewer;
-  kp.Hv = st->known[st->viewer];
-  kp.V0 = st->V;
-  kp.U = st->U;
-  kp.T = st->T;
-  kp.numm = (1u << (2 * st->R)) - 1u;
-  kp.JB = (uint32_t)(2 * st->R);
-  kp.pend0 = st->pend_key >= 0 ? (uint32_t)st->pend_key : kNoKey;
-  kp.corr0 = (uint32_t)st->corr;
-  kp.N = st->N;
-  kp.debug = d->d_debug;
-  kp.table = plan->d_table;
-  kp.plan = plan->d_plan;
+  fill_kparams(kp, st, seed, node_id, (uint32_t)n_actions, plan, d);
   kp.hist = d_hist;
   kp.winners = d_winners;
   kp.trace_stride = (uint32_t)(sim_end - sim_begin);
@@ -316,9 +327,110 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   return DVC_OK;
 }
 
+// Device-resident flat search: the root-expansion batch (the
+// first k children, sims [0, n)) and then ONE cooperative flat_search_kernel
+// for the remaining `iters` UCB1 iterations, all on this thread's stream with
+// a single synchronisation at the end.
+int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, const uint32_t *first, int32_t k,
+                         const int32_t *batch_pos, const double *lnN, int32_t iters, const dvc_search_params *p,
+                         uint64_t *visits, uint64_t *wins) {
+  const State *st = as_state(s);
+  if (!st) return set_err(DVC_E_CONFIG, "bad state");
+  const int P = st->P;
+  const uint64_t n = p->sims_per_child;
+  const size_t nh = (size_t)k * P;
+  const size_t off_delta = (size_t)iters * 8, off_out = off_delta + (size_t)iters * 8,
+               off_bp = off_out + (size_t)A * 16, bytes = off_bp + (size_t)A * 4;
+  DeviceScratch *d = nullptr;
+  HostLane *L = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    int rc = get_scratch(p->device, &d);
+    if (rc) return rc;
+    rc = get_lane(d, nh, &L);
+    if (rc) return rc;
+    if (L->search_cap < bytes) {
+      if (L->d_search) cudaFree(L->d_search);
+      L->d_search = nullptr;
+      L->search_cap = 0;
+      cudaError_t e = cudaMalloc(&L->d_search, bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(search)");
+      L->search_cap = bytes;
+    }
+    cudaError_t e = cudaMemsetAsync(L->d_hist, 0, nh * sizeof(unsigned long long), L->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L->d_search + off_delta, 0, (size_t)iters * 8, L->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(L->d_search, lnN, (size_t)iters * 8, cudaMemcpyHostToDevice, L->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(L->d_search + off_bp, batch_pos, (size_t)A * 4, cudaMemcpyHostToDevice, L->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "search setup");
+  }
+  int rc = enqueue(s, first, k, p->seed, 0u, 0, n, L->d_hist, nullptr, d->device, L->stream, nullptr);
+  if (rc) return rc;
+  KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  const char *err = nullptr;
+  rc = decode_actions(*st, codes, A, kp.meta, &err);
+  if (rc) return set_err(rc, err ? err : "illegal action");
+  std::memcpy(kp.codes, codes, sizeof(uint32_t) * A);
+  std::vector<unsigned long long> out((size_t)A * 2);
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    PlanEntry *plan = nullptr;
+    rc = get_plan(d, *st, L->stream, &plan);
+    if (rc) return rc;
+    fill_kparams(kp, st, p->seed, 0u, (uint32_t)A, plan, d);
+    SearchArgs sa;
+    sa.lnN = reinterpret_cast<const double *>(L->d_search);
+    sa.delta = reinterpret_cast<unsigned long long *>(L->d_search + off_delta);
+    sa.out = reinterpret_cast<unsigned long long *>(L->d_search + off_out);
+    sa.batch_pos = reinterpret_cast<const int32_t *>(L->d_search + off_bp);
+    sa.first_hist = L->d_hist;
+    sa.c = p->c;
+    sa.n = (uint32_t)n;
+    sa.iters = (uint32_t)iters;
+    const int block = 128;
+    const size_t smem = (size_t)A * 16;
+    const uint64_t okey = (3ull << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
+                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)block << 32) | (uint64_t)smem;
+    int per_sm = 0;
+    auto it = d->occupancy.find(okey);
+    if (it != d->occupancy.end()) {
+      per_sm = it->second;
+    } else {
+      cudaError_t e = search_occupancy(P, st->jokers != 0, st->consecutive != 0, block, smem, &per_sm);
+      if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+      d->occupancy[okey] = per_sm;
+    }
+    if (per_sm < 1) return set_err(DVC_E_CONFIG, "search kernel cannot launch");
+    uint64_t grid = (n + block - 1) / block;
+    if (grid > (uint64_t)per_sm * d->num_sms) grid = (uint64_t)per_sm * d->num_sms;
+    cudaError_t e = launch_flat_search(kp, sa, P, st->jokers != 0, st->consecutive != 0, (int)grid, block, smem,
+                                       L->stream);
+    g_launches++;
+    if (e != cudaSuccess) return cuda_fail(e, "flat_search_kernel launch");
+    e = cudaMemcpyAsync(out.data(), sa.out, out.size() * 8, cudaMemcpyDeviceToHost, L->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "search readback");
+  }
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "flat search");
+  for (int32_t a = 0; a < A; ++a) {
+    visits[a] = out[a];
+    wins[a] = out[(size_t)A + a];
+  }
+  return DVC_OK;
+}
+
 }  // namespace
 
 int set_error(int code, const char *msg) { return set_err(code, msg ? msg : ""); }
+
+bool search_on_device() { return g_search_device.load() != 0; }
+
+int flat_search_gpu(const dvc_state *s, const uint32_t *codes, int32_t A, const uint32_t *first, int32_t k,
+                    const int32_t *batch_pos, const double *lnN, int32_t iters, const dvc_search_params *p,
+                    uint64_t *visits, uint64_t *wins) {
+  return flat_search_gpu_impl(s, codes, A, first, k, batch_pos, lnN, iters, p, visits, wins);
+}
 
 }  // namespace dvc
 
@@ -510,6 +622,9 @@ int dvc_set_option(const char *name, int64_t value) {
   } else if (n == "plan_cache") {
     if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "plan_cache must be 0 or 1");
     g_plan_cache = value;
+  } else if (n == "search_device") {
+    if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "search_device must be 0 or 1");
+    g_search_device = value;
   } else {
     return set_err(DVC_E_CONFIG, "unknown option " + n);
   }
@@ -525,6 +640,7 @@ int dvc_get_option(const char *name, int64_t *value) {
   else if (n == "table_cap") *value = g_table_cap;
   else if (n == "plan_cache") *value = g_plan_cache;
   else if (n == "chunk") *value = g_chunk;
+  else if (n == "search_device") *value = g_search_device;
   else return set_err(DVC_E_CONFIG, "unknown option " + n);
   return DVC_OK;
 }
@@ -564,6 +680,7 @@ void dvc_shutdown(void) {
     if (d->d_counters) cudaFree(d->d_counters);
     for (auto &kv2 : d->lanes) {
       if (kv2.second.d_hist) cudaFree(kv2.second.d_hist);
+      if (kv2.second.d_search) cudaFree(kv2.second.d_search);
       if (kv2.second.stream) cudaStreamDestroy(kv2.second.stream);
     }
     delete d;

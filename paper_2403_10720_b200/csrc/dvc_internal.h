@@ -78,6 +78,11 @@ __host__ __device__ inline uint32_t act_meta(uint32_t d, uint32_t pos, uint32_t 
 
 // ---- error reporting (api.cu): sets dvc_last_error(), returns code ----
 int set_error(int code, const char *msg);
+// Device flat search (api.cu): option "search_device", and the call itself.
+bool search_on_device();
+int flat_search_gpu(const dvc_state *s, const uint32_t *codes, int32_t A, const uint32_t *first, int32_t k,
+                    const int32_t *batch_pos, const double *lnN, int32_t iters, const dvc_search_params *p,
+                    uint64_t *visits, uint64_t *wins);
 
 // ---- host functions (host.cpp) ----
 int encode(const dvc_observation *obs, State *st, const char **err);

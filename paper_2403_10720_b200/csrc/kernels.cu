@@ -16,6 +16,7 @@
 // Both rollout kernels reduce winners into shared-memory u32 counters
 // hist[a][w] and flush them with one global atomicAdd(u64) per non-zero
 // counter per block.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include "rollout.cuh"
 
@@ -303,6 +304,129 @@ __global__ void det_table_kernel(const uint8_t *__restrict__ plan, uint64_t N, u
 
 __global__ void add_u64_kernel(unsigned long long *p, uint32_t n, unsigned long long v) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] += v;
+}
+
+// ---- device-resident flat search -------------------------------------------
+// The UCB1 loop of dvc_mcts_search (flat = 1) after the root expansion batch,
+// run on the GPU as ONE cooperative kernel instead of one blocking host round
+// trip per iteration.  Per iteration every block selects the
+// same child redundantly from its shared-memory copy of (visits, wins) --
+// UCB1 in IEEE double with no contraction (__d*_rn), ln(N) from the host's
+// libm table, so the choice is bit-identical to the host loop -- then the grid
+// plays sims [visits, visits + n) of that child, one playout per lane, adds
+// the viewer's wins into delta[it], and a grid barrier publishes the sum.
+__device__ __forceinline__ bool ucb_better(double v, uint32_t code, uint32_t i, double bv, uint32_t bcode,
+                                           uint32_t bi) {
+  if (i == 0xFFFFFFFFu) return false;
+  if (bi == 0xFFFFFFFFu) return true;
+  return v > bv || (v == bv && code < bcode);
+}
+
+template <int P, bool JOK, bool CONS>
+__global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant__ KParams kp,
+                                                          const __grid_constant__ SearchArgs sa) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned long long shs[];
+  unsigned long long *vis = shs, *win = shs + kp.A;
+  __shared__ double red_v[4];
+  __shared__ uint32_t red_i[4], s_best;
+  for (uint32_t a = threadIdx.x; a < kp.A; a += blockDim.x) {
+    const int32_t bp = sa.batch_pos[a];
+    vis[a] = bp >= 0 ? sa.n : 0ull;
+    win[a] = bp >= 0 ? sa.first_hist[(size_t)bp * P + kp.g0] : 0ull;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gsize = gridDim.x * blockDim.x;
+  for (uint32_t it = 0; it < sa.iters; ++it) {
+    // ---- selection (every block, same result)
+    const double lnN = sa.lnN[it];
+    double bv = 0.0;
+    uint32_t bi = 0xFFFFFFFFu, bcode = 0;
+    for (uint32_t a = threadIdx.x; a < kp.A; a += blockDim.x) {
+      const double v = vis[a] == 0 ? (double)INFINITY
+                     : __dadd_rn(__ddiv_rn((double)win[a], (double)vis[a]),
+                                 __dmul_rn(sa.c, __dsqrt_rn(__ddiv_rn(lnN, (double)vis[a]))));
+      if (ucb_better(v, kp.codes[a], a, bv, bcode, bi)) { bv = v; bi = a; bcode = kp.codes[a]; }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const double ov = __shfl_down_sync(0xFFFFFFFFu, bv, off);
+      const uint32_t oi = __shfl_down_sync(0xFFFFFFFFu, bi, off);
+      const uint32_t oc = __shfl_down_sync(0xFFFFFFFFu, bcode, off);
+      if (ucb_better(ov, oc, oi, bv, bcode, bi)) { bv = ov; bi = oi; bcode = oc; }
+    }
+    if (lane == 0) { red_v[wid] = bv; red_i[wid] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) {
+        const uint32_t oi = red_i[w];
+        if (oi != 0xFFFFFFFFu && ucb_better(red_v[w], kp.codes[oi], oi, bv, bcode, bi)) {
+          bv = red_v[w]; bi = oi; bcode = kp.codes[oi];
+        }
+      }
+      s_best = bi;
+    }
+    __syncthreads();
+    const uint32_t best = s_best;
+    const uint32_t code = kp.codes[best], meta = kp.meta[best];
+    const uint32_t sbase = (uint32_t)vis[best];
+    // ---- simulation: sims [visits, visits + n) of the chosen child
+    uint32_t cnt = 0;
+    for (uint32_t i = gtid; i < sa.n; i += gsize) {
+      const uint32_t s = sbase + i;
+      Sim<P> S;
+      uint32_t st = start_playout<P, JOK, CONS, false>(S, s, code, meta, kp);
+      for (uint32_t k = 0; st != FINISH; ++k)
+        st = step_playout<P, JOK, CONS, false>(S, st, k, s, code, nullptr, nullptr, 0, kp);
+      cnt += winner_seat(S) == kp.g0 ? 1u : 0u;
+    }
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (lane == 0 && cnt) atomicAdd(sa.delta + it, (unsigned long long)cnt);
+    // ---- backpropagation, published by the grid barrier
+    grid.sync();
+    if (threadIdx.x == 0) {
+      vis[best] += sa.n;
+      win[best] += __ldcg(sa.delta + it);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0)
+    for (uint32_t a = threadIdx.x; a < kp.A; a += blockDim.x) {
+      sa.out[a] = vis[a];
+      sa.out[kp.A + a] = win[a];
+    }
+}
+
+template <int P, bool JOK, bool CONS>
+const void *search_fn() { return (const void *)flat_search_kernel<P, JOK, CONS>; }
+
+const void *select_search(int P, bool jok, bool cons) {
+#define DVC_SCASE(PP)                                                                            \
+  if (P == PP) {                                                                                 \
+    if (jok) return cons ? search_fn<PP, true, true>() : search_fn<PP, true, false>();          \
+    return cons ? search_fn<PP, false, true>() : search_fn<PP, false, false>();                 \
+  }
+  DVC_SCASE(2)
+  DVC_SCASE(3)
+  DVC_SCASE(4)
+#undef DVC_SCASE
+  return nullptr;
+}
+
+cudaError_t search_occupancy(int P, bool jok, bool cons, int block, size_t smem, int *blocks_per_sm) {
+  const void *f = select_search(P, jok, cons);
+  if (!f) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+}
+
+cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, int grid,
+                               int block, size_t smem, cudaStream_t stream) {
+  const void *f = select_search(P, jok, cons);
+  if (!f) return cudaErrorInvalidValue;
+  void *args[] = {(void *)&kp, (void *)&sa};
+  return cudaLaunchCooperativeKernel(f, grid, block, args, smem, stream);
 }
 
 // ----------------------------------------------------------------- launchers

@@ -122,6 +122,23 @@ int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p,
   return DVC_OK;
 }
 
+// Move choice (most visits, then most wins, then smallest code) and
+// the per-child table.
+int finish(const std::vector<uint32_t> &codes, const std::vector<uint64_t> &visits,
+           const std::vector<uint64_t> &wins, dvc_action_stat *table, uint32_t *best_code) {
+  const int A = (int)codes.size();
+  int bi = 0;
+  for (int a = 1; a < A; ++a) {
+    if (visits[a] > visits[bi] || (visits[a] == visits[bi] &&
+        (wins[a] > wins[bi] || (wins[a] == wins[bi] && codes[a] < codes[bi])))) bi = a;
+  }
+  for (int a = 0; a < A; ++a) {
+    table[a].code = codes[a]; table[a]._pad = 0; table[a].visits = visits[a]; table[a].wins = wins[a];
+  }
+  if (best_code) *best_code = codes[bi];
+  return DVC_OK;
+}
+
 }  // namespace
 
 extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table,
@@ -158,6 +175,20 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     std::sort(order.begin(), order.end(), [&](int x, int y) { return codes[x] < codes[y]; });
     std::vector<uint32_t> first((size_t)k);
     for (int i = 0; i < k; ++i) first[i] = codes[order[i]];
+    const int iters = p->expansions - k;
+    if (iters > 0 && search_on_device() && n * (uint64_t)(iters + 1) <= (1ull << 32)) {
+      // The whole search on the GPU (api.cu flat_search_gpu): the same
+      // selections and playouts as the host loop below, without a host round
+      // trip per iteration.  ln(N) comes from this host's libm, N = (k + it) n.
+      std::vector<int32_t> batch_pos((size_t)A, -1);
+      for (int i = 0; i < k; ++i) batch_pos[order[i]] = i;
+      std::vector<double> lnN((size_t)iters);
+      for (int i = 0; i < iters; ++i) lnN[i] = std::log((double)((uint64_t)(k + i) * n));
+      int rc = flat_search_gpu(s, codes.data(), A, first.data(), k, batch_pos.data(), lnN.data(), iters, p,
+                               visits.data(), wins.data());
+      if (rc) return rc;
+      return finish(codes, visits, wins, table, best_code);
+    }
     std::vector<uint64_t> h((size_t)k * st->P);
     int rc = dvc_rollout_batch_ex(s, first.data(), k, p->seed, 0u, 0, n, h.data(), nullptr, p->device);
     if (rc) return rc;
@@ -192,14 +223,5 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     wins[best] += hist[st->viewer];
     N += n;
   }
-  int bi = 0;
-  for (int a = 1; a < A; ++a) {
-    if (visits[a] > visits[bi] || (visits[a] == visits[bi] &&
-        (wins[a] > wins[bi] || (wins[a] == wins[bi] && codes[a] < codes[bi])))) bi = a;
-  }
-  for (int a = 0; a < A; ++a) {
-    table[a].code = codes[a]; table[a]._pad = 0; table[a].visits = visits[a]; table[a].wins = wins[a];
-  }
-  if (best_code) *best_code = codes[bi];
-  return DVC_OK;
+  return finish(codes, visits, wins, table, best_code);
 }

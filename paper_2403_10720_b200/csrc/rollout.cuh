@@ -53,6 +53,18 @@ struct KParams {
   uint32_t meta[kMaxActions];   // act_meta(d, pos, v); d = 0 -> STOP
 };
 
+// Device flat search (kernels.cu flat_search_kernel).
+struct SearchArgs {
+  const double *lnN;                     // [iters] log(N) before iteration it (host libm)
+  const int32_t *batch_pos;              // [A] row of child a in the root-expansion batch, -1 if none
+  const unsigned long long *first_hist;  // [k * P] that batch's winner histogram
+  unsigned long long *delta;             // [iters] viewer wins of iteration it (zeroed)
+  unsigned long long *out;               // [2 * A] final visits, then wins
+  double c;                              // UCB1 constant
+  uint32_t n;                            // sims per iteration
+  uint32_t iters;                        // iterations after the root expansion
+};
+
 // ----------------------------------------------------------------- RNG (§R3)
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                                uint32_t k0, uint32_t k1) {

@@ -128,3 +128,8 @@ def test_options_roundtrip(dvc):
         dvc.set_option("block", 1025)
     with pytest.raises(dvc.DvcError):
         dvc.set_option("nope", 1)
+    assert dvc.get_option("search_device") == 0            # host tree by default (north_star)
+    with dvc.options(search_device=1):
+        assert dvc.get_option("search_device") == 1
+    with pytest.raises(dvc.DvcError):
+        dvc.set_option("search_device", 2)

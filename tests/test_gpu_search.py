@@ -41,6 +41,33 @@ def test_flat_search_equals_oracle(dvc, oracle_lib, path):
     assert stats_d == stats_o and best_d == best_o
 
 
+DEVICE_CASES = [("fixtures/c3_d1.json", 96, 1000), ("fixtures/c2_d2.json", 80, 4097),
+                ("tests/golden/T2c1.json", 300, 128), ("fixtures/x3_d1.json", 70, 333),
+                ("fixtures/xsmall_d3.json", 40, 20000), ("fixtures/c4_d2.json", 140, 200)]
+
+
+@pytest.mark.parametrize("path,exp_n,n", DEVICE_CASES, ids=[os.path.basename(c[0]) for c in DEVICE_CASES])
+def test_device_search_loop_equals_host_loop_and_oracle(dvc, oracle_lib, path, exp_n, n):
+    """The cooperative flat_search_kernel (search_device=1: UCB1 selection,
+    playouts and backpropagation on the GPU, grid barrier per iteration) gives
+    the same table as the host loop (search_device=0) and the oracle's
+    flat_search, over budgets that run many iterations after the root
+    expansion, with n not a multiple of the block and grids of several blocks."""
+    from oracle.search import flat_search
+    d = json.load(open(os.path.join(ROOT, path)))
+    st = dvc.encode(d)
+    assert exp_n > len(st.legal_actions())          # iterations remain after the root expansion
+    with dvc.options(search_device=1):
+        best_dev, stats_dev = dvc.mcts_search(st, exp_n, n, 77)
+    with dvc.options(search_device=0):
+        best_host, stats_host = dvc.mcts_search(st, exp_n, n, 77)
+    stats_dev = [tuple(map(int, t)) for t in stats_dev]
+    assert stats_dev == [tuple(map(int, t)) for t in stats_host] and best_dev == best_host
+    best_o, stats_o = flat_search(d, exp_n, n, 77)
+    assert stats_dev == stats_o and best_dev == best_o
+    assert sum(v for _, v, _ in stats_dev) == exp_n * n
+
+
 def test_search_errors(dvc):
     d = json.load(open(os.path.join(ROOT, "fixtures", "c2_d1.json")))
     st = dvc.encode(d)

@@ -82,7 +82,10 @@ def main():
         # full self-play games (2p, 26 tiles with jokers), every decision a
         # dvc_mcts_search of 64 expansions x 1024 playouts per child
         from paper_2403_10720_b200.selfplay import play_game
-        for flat, label in ((1, "flat UCT (root-parallel, PAPER:180)"), (0, "depth-capped tree, max_depth 4")):
+        for flat, sdev, label in ((1, 1, "flat UCT (root-parallel, PAPER:180), device-resident UCB loop"),
+                                  (1, 0, "flat UCT (root-parallel, PAPER:180), host UCB loop"),
+                                  (0, 0, "depth-capped tree, max_depth 4")):
+            dvc.set_option("search_device", sdev)
             rows = []
             dvc.mcts_search(dvc.encode(load("c3_d*.json")[0]), 4, 1024, 5, flat=flat)
             for g in range(4):
@@ -105,6 +108,7 @@ def main():
                               "concurrent_16_games": {"decisions": sum(g["decisions"] for g in many), "s": round(tm, 3),
                                                       "decisions_per_s": sum(g["decisions"] for g in many) / tm}}),
                   flush=True)
+        dvc.set_option("search_device", 0)
     if "c4" in todo:
         rows = []
         for i, d in enumerate(load("c4_d*.json")):
