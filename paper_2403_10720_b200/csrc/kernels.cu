@@ -89,12 +89,11 @@ __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_
   return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
 }
 
-// Decision step k of a running playout (a4).
+// Decision step k of a running playout (a4), given its Philox block B_k.
 template <int P, bool JOK, bool CONS, bool PATH>
-__device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
-                                                 const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
-                                                 const KParams &kp) {
-  const uint4 B = philox_rk(k, s, code, kp.node, kp);
+__device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint4 B, uint32_t k,
+                                               const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
+                                               const KParams &kp) {
   turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
 #ifdef DVC_DEBUG
   dbg_check_state<P, JOK>(S, kp);
@@ -132,6 +131,13 @@ __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_
 #else
   return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
 #endif
+}
+
+template <int P, bool JOK, bool CONS, bool PATH>
+__device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
+                                                 const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
+                                                 const KParams &kp) {
+  return step_block<P, JOK, CONS, PATH>(S, st, philox_rk(k, s, code, kp.node, kp), k, meta_of_a, path_of, a, kp);
 }
 
 template <int P, bool JOK, bool CONS, bool PATH>
@@ -378,8 +384,14 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
       const uint32_t s = sbase + i;
       Sim<P> S;
       uint32_t st = start_playout<P, JOK, CONS, false>(S, s, code, meta, kp);
-      for (uint32_t k = 0; st != FINISH; ++k)
-        st = step_playout<P, JOK, CONS, false>(S, st, k, s, code, nullptr, nullptr, 0, kp);
+      // latency-bound loop: B_{k+1} is independent of the state, so it is
+      // generated while step k runs
+      uint4 B = philox_rk(0u, s, code, kp.node, kp);
+      for (uint32_t k = 0; st != FINISH; ++k) {
+        const uint4 Bn = philox_rk(k + 1u, s, code, kp.node, kp);
+        st = step_block<P, JOK, CONS, false>(S, st, B, k, nullptr, nullptr, 0, kp);
+        B = Bn;
+      }
       cnt += winner_seat(S) == kp.g0 ? 1u : 0u;
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
