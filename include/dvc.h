@@ -140,6 +140,21 @@ int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t
                             uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
                             uint64_t *d_hist, uint64_t *d_visits, int32_t device, void *cuda_stream);
 
+/* Common random numbers across actions (DESIGN.md §R3
+ * "CRN"): as dvc_rollout_batch_ex / dvc_rollout_batch_async, except that the
+ * determinization block of sim s is D = Philox(ctr = (0xFFFFFFFF, s,
+ * 0xFFFFFFFE, node_id)) for EVERY action, so all actions of the batch play
+ * against the same hidden-tile assignment for each sim index (the decision
+ * blocks B_t stay keyed by the action code).  Differences between actions
+ * then have lower variance; each action's counts alone have the same
+ * distribution as without CRN.  hist is HOST (_ex) or DEVICE, added to (_async). */
+int dvc_rollout_batch_crn_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
+                             int32_t device);
+int dvc_rollout_batch_crn_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                                uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
+                                int32_t device, void *cuda_stream);
+
 /* Debug/parity form of the async call: additionally writes the winner seat of
  * every playout to d_winners[a*(sim_end-sim_begin) + (s - sim_begin)] (DEVICE,
  * uint8).  Same kernels and launch configuration as the async call. */

@@ -53,6 +53,7 @@ def lib():
         L.oracle_unrank.argtypes = [P(I32), U64, P(I32), I32, P(I32)]
         L.oracle_legal.argtypes = [P(I32), P(U32), I32, P(I32)]
         L.oracle_rollout.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64)]
+        L.oracle_rollout_crn.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64), I32]
         L.oracle_playout.argtypes = [P(I32), U32, U64, U32, U32, P(I32)]
         L.oracle_rollout_path.argtypes = [P(I32), P(U32), I32, P(U32), I32, U64, U32, U64, U64, P(U64), P(U64)]
         _lib = L
@@ -110,13 +111,14 @@ def legal(obs_json):
     return list(buf[:n.value])
 
 
-def rollout(obs_json, codes, seed, node_id, s0, s1):
-    """hist[a][w] (list of lists) for sims [s0, s1)."""
+def rollout(obs_json, codes, seed, node_id, s0, s1, crn=False):
+    """hist[a][w] (list of lists) for sims [s0, s1); crn = common
+    determinizations across actions."""
     P = int(obs_json["rules"]["players"])
     A = len(codes)
     c = (ctypes.c_uint32 * max(A, 1))(*codes)
     h = (ctypes.c_uint64 * max(A * P, 1))()
-    _check(lib().oracle_rollout(flatten(obs_json), c, A, seed, node_id, s0, s1, h))
+    _check(lib().oracle_rollout_crn(flatten(obs_json), c, A, seed, node_id, s0, s1, h, 1 if crn else 0))
     return [list(h[a * P:(a + 1) * P]) for a in range(A)]
 
 

@@ -446,11 +446,12 @@ class DetSpace:
 
 # ----------------------------------------------------------------- playout (§R5)
 
-def playout(space, code, seed, node_id, s, trace=None):
+def playout(space, code, seed, node_id, s, trace=None, crn=False):
     """One playout: determinize with block D, apply the root action, then play
     uniformly random decisions with one Philox block per decision step.
-    Returns the winner seat."""
-    D = px.det_block(seed, node_id, code, s)
+    Returns the winner seat.  crn: D is keyed by CRN_WORD instead of the code
+    (common determinizations across actions)."""
+    D = px.det_block(seed, node_id, px.CRN_WORD if crn else code, s)
     rho = px.rank64(space.N, D[0], D[1])
     game = space.game(space.unrank(rho))
     step = game.apply(code)
@@ -521,7 +522,7 @@ def check_action(obs, code):
         raise ValueError("illegal action %08x" % code)
 
 
-def rollout(obs, codes, seed, node_id, s0, s1):
+def rollout(obs, codes, seed, node_id, s0, s1, crn=False):
     """hist[a][w] over sims s in [s0, s1) (§R6)."""
     space = DetSpace(obs)
     if space.N == 0:
@@ -531,5 +532,5 @@ def rollout(obs, codes, seed, node_id, s0, s1):
     hist = [[0] * obs.rules.P for _ in codes]
     for ai, c in enumerate(codes):
         for s in range(s0, s1):
-            hist[ai][playout(space, c, seed, node_id, s)] += 1
+            hist[ai][playout(space, c, seed, node_id, s, crn=crn)] += 1
     return hist

@@ -362,10 +362,14 @@ void root_legal(const Obs &o, std::vector<u32> &out) {
 
 // One playout (§R5): determinize with block D, apply the root action, then one
 // Philox block per decision step.  Returns the winner; *steps = #decisions.
+// crn: D keyed by CRN_WORD instead of the code (common determinizations
+// across actions).
+const u32 CRN_WORD = 0xFFFFFFFEu;
+
 int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
-            std::vector<u32> &L) {
+            std::vector<u32> &L, bool crn = false) {
   u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
-  Block D = philox(0xFFFFFFFFu, s, code, node, k0, k1);
+  Block D = philox(0xFFFFFFFFu, s, crn ? CRN_WORD : code, node, k0, k1);
   u64 rho = rank64(sp.N, D.v[0], D.v[1]);
   Game G = sp.game(sp.unrank(rho));
   Game::Step st = G.apply(code);
@@ -458,8 +462,8 @@ int oracle_legal(const int32_t *obs, uint32_t *codes, int32_t cap, int32_t *n_ou
 }
 
 // hist[a*P + w] += #playouts s in [s0, s1) of action a won by seat w
-int oracle_rollout(const int32_t *obs, const uint32_t *codes, int32_t n_codes, uint64_t seed,
-                   uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist) {
+int oracle_rollout_crn(const int32_t *obs, const uint32_t *codes, int32_t n_codes, uint64_t seed,
+                       uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist, int32_t crn) {
   try {
     Obs o = parse(obs);
     DetSpace sp(o);
@@ -471,9 +475,14 @@ int oracle_rollout(const int32_t *obs, const uint32_t *codes, int32_t n_codes, u
     int P = o.rules.P;
     for (int a = 0; a < n_codes; ++a)
       for (u64 s = s0; s < s1; ++s)
-        hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L)] += 1;
+        hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L, crn != 0)] += 1;
     return 0;
   } catch (std::exception &e) { g_err = e.what(); return -1; }
+}
+
+int oracle_rollout(const int32_t *obs, const uint32_t *codes, int32_t n_codes, uint64_t seed,
+                   uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist) {
+  return oracle_rollout_crn(obs, codes, n_codes, seed, node, s0, s1, hist, 0);
 }
 
 // deep-tree batch: hist[a*P + w], voids[a] for forced path + codes[a]

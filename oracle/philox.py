@@ -22,6 +22,11 @@ PHILOX_W0 = 0x9E3779B9
 PHILOX_W1 = 0xBB67AE85
 
 DET_CTR_X = 0xFFFFFFFF  # counter word x of the determinization block (§R3)
+# Common-random-numbers variant: the
+# determinization block takes this word in place of the action code, so every
+# action of a batch sees the same hidden-tile assignment for a given sim index.
+# 0xFFFFFFFE is no action code (targets are <= 3, STOP is 0xFFFFFFFF).
+CRN_WORD = 0xFFFFFFFE
 
 
 def philox4x32_10(ctr, key):

@@ -224,6 +224,7 @@ struct PathArg {
   const uint32_t *codes = nullptr;
   int32_t len = 0;
   unsigned long long *d_voids = nullptr;
+  bool crn = false;         // common random numbers across actions (root batches only)
 };
 
 int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed, uint32_t node_id,
@@ -267,6 +268,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   fill_kparams(kp, st, seed, node_id, (uint32_t)n_actions, plan, d);
   kp.hist = d_hist;
   kp.winners = d_winners;
+  kp.crn = path.crn ? 1u : 0u;
   kp.trace_stride = (uint32_t)(sim_end - sim_begin);
   kp.trace_s0 = (uint32_t)sim_begin;
 
@@ -466,9 +468,13 @@ int dvc_legal_actions(const dvc_state *s, uint32_t *codes, int32_t cap, int32_t 
   return DVC_OK;
 }
 
-int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
-                         uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
-                         uint64_t *visits, int32_t device) {
+}  // extern "C"
+
+namespace dvc {
+namespace {
+int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                     uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist, uint64_t *visits,
+                     int32_t device, bool crn) {
   if (!hist) return set_err(DVC_E_CONFIG, "hist is null");
   const State *st = s ? as_state(s) : nullptr;
   if (!st) return set_err(DVC_E_CONFIG, "bad state");
@@ -495,8 +501,10 @@ int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_
     cudaError_t e = cudaMemsetAsync(L->d_hist, 0, n * sizeof(unsigned long long), L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
   }
+  PathArg opt;
+  opt.crn = crn;
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
-                   L->stream, nullptr);
+                   L->stream, nullptr, opt);
   if (rc) return rc;
   std::vector<unsigned long long> tmp(n);
   cudaError_t e = cudaMemcpyAsync(tmp.data(), L->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -507,6 +515,48 @@ int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_
   if (visits)
     for (int a = 0; a < n_actions; ++a) visits[a] = sim_end - sim_begin;
   return DVC_OK;
+}
+
+int rollout_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                  uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist, uint64_t *d_visits,
+                  int32_t device, void *cuda_stream, bool crn) {
+  if (!d_hist) return set_err(DVC_E_CONFIG, "d_hist is null");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  PathArg opt;
+  opt.crn = crn;
+  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
+                   reinterpret_cast<unsigned long long *>(d_hist), nullptr, device, stream, nullptr, opt);
+  if (rc) return rc;
+  if (d_visits) {
+    cudaError_t e = launch_add_u64(reinterpret_cast<unsigned long long *>(d_visits), (uint32_t)n_actions,
+                                   sim_end - sim_begin, stream);
+    g_launches++;
+    if (e != cudaSuccess) return cuda_fail(e, "visits");
+  }
+  return DVC_OK;
+}
+}  // namespace
+}  // namespace dvc
+
+extern "C" {
+
+int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                         uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
+                         uint64_t *visits, int32_t device) {
+  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, visits, device, false);
+}
+
+int dvc_rollout_batch_crn_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
+                             int32_t device) {
+  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, true);
+}
+
+int dvc_rollout_batch_crn_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                                uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
+                                int32_t device, void *cuda_stream) {
+  return rollout_async(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d_hist, nullptr, device,
+                       cuda_stream, true);
 }
 
 int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_len, const uint32_t *actions,
@@ -578,18 +628,8 @@ int dvc_rollout_batch(const dvc_state *s, const uint32_t *actions, int32_t n_act
 int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
                             uint64_t *d_visits, int32_t device, void *cuda_stream) {
-  if (!d_hist) return set_err(DVC_E_CONFIG, "d_hist is null");
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
-  int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
-                   reinterpret_cast<unsigned long long *>(d_hist), nullptr, device, stream, nullptr);
-  if (rc) return rc;
-  if (d_visits) {
-    cudaError_t e = launch_add_u64(reinterpret_cast<unsigned long long *>(d_visits), (uint32_t)n_actions,
-                                   sim_end - sim_begin, stream);
-    g_launches++;
-    if (e != cudaSuccess) return cuda_fail(e, "visits");
-  }
-  return DVC_OK;
+  return rollout_async(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d_hist, d_visits, device,
+                       cuda_stream, false);
 }
 
 int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,

@@ -79,7 +79,7 @@ __device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P,
 template <int P, bool JOK, bool CONS, bool PATH>
 __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t code, uint32_t meta,
                                                   const KParams &kp) {
-  const uint4 D = philox_rk(0xFFFFFFFFu, s, code, kp.node, kp);
+  const uint4 D = philox_rk(0xFFFFFFFFu, s, kp.crn ? kCrnWord : code, kp.node, kp);
   determinize<P>(S, D, kp);
   uint32_t t;
   bool correct;

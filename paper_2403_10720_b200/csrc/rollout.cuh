@@ -17,6 +17,7 @@ namespace dvc {
 constexpr int kMaxActions = 768;
 
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
+constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's counter word z under common random numbers (no action code)
 
 struct KParams {
   uint32_t k0, k1;        // Philox key = (lo32(seed), hi32(seed))
@@ -38,6 +39,7 @@ struct KParams {
   uint64_t N;             // |Det(O)|
   uint64_t div_magic;     // ceil(2^64 / n_per) (0 when n_per == 1): item / n_per = umul64hi(item, magic)
   uint32_t nb;            // refill kernel: kBatch-sized sim batches per action = ceil(n_per / kBatch)
+  uint32_t crn;           // 1: determinization block keyed by kCrnWord, not the action code (§R3 CRN)
   uint32_t rk[20];        // Philox round keys (k0 + r*W0, k1 + r*W1), r = 0..9: read from the
                           // constant bank as instruction operands (no registers, no adds)
   const uint4 *table;     // N entries (H1, H2, H3, jinfo) or null -> inline unrank

@@ -29,9 +29,11 @@ def merge_hist(hist, group=None):
     return hist
 
 
-def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None, stream=None):
+def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None, stream=None,
+                         crn=False):
     """Sharded rollout; returns the merged int64 [A, P] histogram ON DEVICE
-    (every rank holds the same totals after the all_reduce)."""
+    (every rank holds the same totals after the all_reduce).  crn: common
+    determinizations across actions."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     s0, s1 = shard_range(n_sims, rank, world)
@@ -39,13 +41,13 @@ def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, 
     hist = torch.zeros((len(actions), state.players), dtype=torch.int64, device=dev)
     if s1 > s0:
         dvc.rollout_batch_async(state, actions, seed, node_id, sim_offset + s0, sim_offset + s1, hist,
-                                stream=stream)
+                                stream=stream, crn=crn)
     return merge_hist(hist, group)
 
 
-def rollout_batch(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None):
+def rollout_batch(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=None, crn=False):
     """As rollout_batch_device, read back to host (numpy-compatible int64 tensor)."""
-    return rollout_batch_device(state, actions, n_sims, seed, node_id, sim_offset, group).cpu()
+    return rollout_batch_device(state, actions, n_sims, seed, node_id, sim_offset, group, crn=crn).cpu()
 
 
 def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, group=None):

@@ -25,7 +25,8 @@ HIDDEN = 0xFF
 
 # every symbol include/dvc.h declares
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
-           "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async", "dvc_mcts_search",
+           "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async",
+           "dvc_rollout_batch_crn_ex", "dvc_rollout_batch_crn_async", "dvc_mcts_search",
            "dvc_set_option", "dvc_get_option", "dvc_debug_counters", "dvc_launch_count", "dvc_last_error",
            "dvc_shutdown"]
 
@@ -97,6 +98,8 @@ def lib():
                                           I32]
         L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
+        L.dvc_rollout_batch_crn_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, P(U64), I32]
+        L.dvc_rollout_batch_crn_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, I32, VP]
         L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
         L.dvc_debug_counters.argtypes = [I32, P(U32)]
         L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
@@ -200,13 +203,19 @@ def rollout_batch(state, actions, n_sims, seed):
     return wins
 
 
-def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-1):
-    """hist[a, w] (numpy uint64, host) for sims [sim_begin, sim_end) (blocking)."""
+def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-1, crn=False):
+    """hist[a, w] (numpy uint64, host) for sims [sim_begin, sim_end) (blocking).
+    crn: common determinizations across actions (dvc_rollout_batch_crn_ex)."""
     a, ap = _codes(actions)
     P = state.players
     hist = np.zeros((len(a), P), dtype=np.uint64)
-    _check(lib().dvc_rollout_batch_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
-                                      hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), None, device))
+    hp = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    if crn:
+        _check(lib().dvc_rollout_batch_crn_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
+                                              hp, device))
+    else:
+        _check(lib().dvc_rollout_batch_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
+                                          hp, None, device))
     return hist
 
 
@@ -230,11 +239,20 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist, visits=None, stream=None):
+def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist, visits=None, stream=None,
+                        crn=False):
     """ADD counts into device tensors hist[A, P] (torch.int64, CUDA) and
-    visits[A] (optional) on `stream` (default: torch's current stream)."""
+    visits[A] (optional) on `stream` (default: torch's current stream).
+    crn: common determinizations across actions (dvc_rollout_batch_crn_async;
+    visits must then be None)."""
     a, ap = _codes(actions)
     dev = hist.device.index
+    if crn:
+        if visits is not None:
+            raise ValueError("the CRN entry point takes no visits array")
+        _check(lib().dvc_rollout_batch_crn_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin,
+                                                 sim_end, ctypes.c_void_p(hist.data_ptr()), dev, _stream_ptr(stream)))
+        return
     _check(lib().dvc_rollout_batch_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                          ctypes.c_void_p(hist.data_ptr()),
                                          ctypes.c_void_p(visits.data_ptr()) if visits is not None else None,

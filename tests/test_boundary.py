@@ -133,3 +133,13 @@ def test_options_roundtrip(dvc):
         assert dvc.get_option("search_device") == 1
     with pytest.raises(dvc.DvcError):
         dvc.set_option("search_device", 2)
+
+
+def test_every_export_has_argtypes(dvc):
+    """Every C-ABI entry point the binding uses declares its argument types
+    (ctypes would otherwise pass 64-bit arguments as C ints)."""
+    L = dvc.lib()
+    for name in dvc.EXPORTS:
+        if name in ("dvc_last_error", "dvc_shutdown"):
+            continue
+        assert getattr(L, name).argtypes is not None, name

@@ -208,3 +208,40 @@ def test_full_size_c2_bench_config(dvc, oracle_lib):
 def test_full_size_c4_sampled(dvc, oracle_lib):
     """BASELINE configs[3] shape on one GPU: 4p/26 tiles, ~1e8 playouts per move."""
     _sampled_full_size(dvc, oracle_lib, "c4_d1.json", 1000000, 400)
+
+
+# ---- common random numbers across actions (DESIGN.md §R3 CRN, SURVEY §8(f) N4)
+CRN_CASES = ["tests/golden/E2.json", "tests/golden/T1.json", "tests/golden/J1.json", "fixtures/c1_d1.json",
+             "fixtures/c2_d3.json", "fixtures/c3_d2.json", "fixtures/x3_d2.json", "fixtures/c4_d3.json",
+             "fixtures/xc0_d1.json"]
+
+
+@pytest.mark.parametrize("kernel", [0, 1], ids=["refill", "naive"])
+@pytest.mark.parametrize("path", CRN_CASES, ids=[os.path.basename(p) for p in CRN_CASES])
+def test_crn_equals_oracle(dvc, oracle_lib, path, kernel):
+    d = load(os.path.join(ROOT, path))
+    st = dvc.encode(d)
+    codes = st.legal_actions()[:12]
+    n = 400 if d["rules"]["players"] < 4 else 150
+    exp = oracle_lib.rollout(d, codes, 31, 2, 17, 17 + n, crn=True)
+    with dvc.options(kernel=kernel):
+        got = dvc.rollout_batch_ex(st, codes, 31, 2, 17, 17 + n, crn=True).astype(np.int64).tolist()
+        hist = torch.zeros((len(codes), st.players), dtype=torch.int64, device="cuda")
+        dvc.rollout_batch_async(st, codes, 31, 2, 17, 17 + n, hist, crn=True)
+        torch.cuda.synchronize()
+    assert got == exp
+    assert hist.cpu().tolist() == exp
+    # a different determinization stream than the default keying
+    assert dvc.rollout_batch_ex(st, codes, 31, 2, 17, 17 + n).astype(np.int64).tolist() != exp or len(codes) == 1
+
+
+def test_crn_e2_complementary_at_full_size(dvc):
+    """E2 at 10^6 sims per action: under CRN exactly one of the two guesses
+    wins each sim (closed form, tests/test_oracle_crn.py), at any size."""
+    d = load(os.path.join(ROOT, "tests", "golden", "E2.json"))
+    st = dvc.encode(d)
+    codes = st.legal_actions()
+    assert len(codes) == 2
+    h = dvc.rollout_batch_ex(st, codes, 5, 0, 0, 1000000, crn=True).astype(np.int64)
+    assert int(h[0, 0] + h[1, 0]) == 1000000
+    assert abs(int(h[0, 0]) - 500000) < 5 * 500                       # p = 1/2, 5 sigma
