@@ -53,7 +53,7 @@ def lib():
         L.oracle_unrank.argtypes = [P(I32), U64, P(I32), I32, P(I32)]
         L.oracle_legal.argtypes = [P(I32), P(U32), I32, P(I32)]
         L.oracle_rollout.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64)]
-        L.oracle_rollout_crn.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64), I32]
+        L.oracle_rollout_flags.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64), I32]
         L.oracle_playout.argtypes = [P(I32), U32, U64, U32, U32, P(I32)]
         L.oracle_rollout_path.argtypes = [P(I32), P(U32), I32, P(U32), I32, U64, U32, U64, U64, P(U64), P(U64)]
         _lib = L
@@ -111,14 +111,16 @@ def legal(obs_json):
     return list(buf[:n.value])
 
 
-def rollout(obs_json, codes, seed, node_id, s0, s1, crn=False):
+def rollout(obs_json, codes, seed, node_id, s0, s1, crn=False, informed=False):
     """hist[a][w] (list of lists) for sims [s0, s1); crn = common
-    determinizations across actions."""
+    determinizations across actions; informed = order-aware
+    playout policy (§R10)."""
     P = int(obs_json["rules"]["players"])
     A = len(codes)
     c = (ctypes.c_uint32 * max(A, 1))(*codes)
     h = (ctypes.c_uint64 * max(A * P, 1))()
-    _check(lib().oracle_rollout_crn(flatten(obs_json), c, A, seed, node_id, s0, s1, h, 1 if crn else 0))
+    flags = (1 if crn else 0) | (2 if informed else 0)
+    _check(lib().oracle_rollout_flags(flatten(obs_json), c, A, seed, node_id, s0, s1, h, flags))
     return [list(h[a * P:(a + 1) * P]) for a in range(A)]
 
 

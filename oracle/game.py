@@ -25,6 +25,7 @@ in left-to-right order; the pool is a sorted list of keys.  Keys: numbered tile
 from . import philox as px
 
 STOP = 0xFFFFFFFF
+BIG = 1 << 30      # "no revealed numbered tile on this side" (order_bounds)
 NONE = -1
 
 
@@ -175,7 +176,10 @@ class Game:
         raise AssertionError("no hidden tile")
 
     # --- legal guesses (§R5 LEGAL)
-    def legal(self):
+    def legal(self, informed=False):
+        """LEGAL(g) (§R5); informed: the order-aware policy list (§R10) -- a
+        numbered value must lie strictly between the nearest revealed numbered
+        tiles left and right of the slot; a joker value is always kept."""
         P, g = self.rules.P, self.g
         own = self.hand(g)
         rev = self.revealed_keys()
@@ -188,13 +192,32 @@ class Game:
                 if r:
                     continue
                 c = colour(k)
+                if informed:
+                    lo, hi = self.order_bounds(j, pos)
                 for v in self.rules.tiles():
                     if colour(v) != c:
                         continue
                     if v in own or v in rev:
                         continue
+                    if informed and not self.rules.is_joker(v) and not (lo < v < hi):
+                        continue
                     out.append(action_code(j, pos, v))
         return out
+
+    def order_bounds(self, j, pos):
+        """(lo, hi): keys of the nearest revealed numbered tiles left and right
+        of position pos in line j, -1 / BIG when there is none (§R10).  The
+        revealed numbered keys increase along a line, so the last one on the
+        left is the largest and the first one on the right the smallest."""
+        lo, hi = -1, BIG
+        for p, (k, r) in enumerate(self.lines[j]):
+            if not r or self.rules.is_joker(k):
+                continue
+            if p < pos:
+                lo = k
+            elif p > pos and hi == BIG:
+                hi = k
+        return lo, hi
 
     def n_choices(self, legal):
         stop = 1 if (self.rules.consecutive and self.corr >= 1) else 0
@@ -247,10 +270,11 @@ class Game:
             self.pend = t
 
 
-def root_legal(obs):
-    """LEGAL(g0) under the viewer's information, plus STOP when allowed (§R5)."""
+def root_legal(obs, informed=False):
+    """LEGAL(g0) under the viewer's information, plus STOP when allowed (§R5);
+    informed: the order-aware list (§R10)."""
     g = _public_game(obs)
-    codes = g.legal()
+    codes = g.legal(informed)
     if obs.rules.consecutive and obs.corr >= 1:
         codes.append(STOP)
     return codes
@@ -446,11 +470,12 @@ class DetSpace:
 
 # ----------------------------------------------------------------- playout (§R5)
 
-def playout(space, code, seed, node_id, s, trace=None, crn=False):
+def playout(space, code, seed, node_id, s, trace=None, crn=False, informed=False):
     """One playout: determinize with block D, apply the root action, then play
     uniformly random decisions with one Philox block per decision step.
     Returns the winner seat.  crn: D is keyed by CRN_WORD instead of the code
-    (common determinizations across actions)."""
+    (common determinizations across actions); informed: every
+    decision is uniform over the order-aware list (§R10) instead of LEGAL."""
     D = px.det_block(seed, node_id, px.CRN_WORD if crn else code, s)
     rho = px.rank64(space.N, D[0], D[1])
     game = space.game(space.unrank(rho))
@@ -465,7 +490,7 @@ def playout(space, code, seed, node_id, s, trace=None, crn=False):
         B = px.step_block(seed, node_id, code, s, k)
         if step == "END_TURN":
             game.start_turn(B[0], B[1])
-        L = game.legal()
+        L = game.legal(informed)
         n = game.n_choices(L)
         i = px.choose(n, B[2])
         k += 1
@@ -522,7 +547,7 @@ def check_action(obs, code):
         raise ValueError("illegal action %08x" % code)
 
 
-def rollout(obs, codes, seed, node_id, s0, s1, crn=False):
+def rollout(obs, codes, seed, node_id, s0, s1, crn=False, informed=False):
     """hist[a][w] over sims s in [s0, s1) (§R6)."""
     space = DetSpace(obs)
     if space.N == 0:
@@ -532,5 +557,5 @@ def rollout(obs, codes, seed, node_id, s0, s1, crn=False):
     hist = [[0] * obs.rules.P for _ in codes]
     for ai, c in enumerate(codes):
         for s in range(s0, s1):
-            hist[ai][playout(space, c, seed, node_id, s, crn=crn)] += 1
+            hist[ai][playout(space, c, seed, node_id, s, crn=crn, informed=informed)] += 1
     return hist

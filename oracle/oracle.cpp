@@ -116,7 +116,9 @@ struct Game {
   // LEGAL(g): opponents in seat order after g, hidden positions left to right,
   // values of the slot's colour in ascending key order (joker last), excluding
   // the mover's own tiles and every revealed tile.
-  void legal(std::vector<u32> &out) const {
+  // informed: keep a numbered value only if it lies strictly
+  // between the nearest revealed numbered tiles left and right of the slot.
+  void legal(std::vector<u32> &out, bool informed = false) const {
     out.clear();
     int P = rules.P, T = n_tiles(rules);
     // excluded[v]: v is in the mover's line or revealed in any line
@@ -130,9 +132,19 @@ struct Game {
         const Tile &t = lines[j][pos];
         if (t.rev) continue;
         int c = colour(t.key);
+        int lo = -1, hi = 1 << 30;
+        if (informed) {
+          for (size_t x = 0; x < lines[j].size(); ++x) {
+            const Tile &u = lines[j][x];
+            if (!u.rev || is_joker(rules, u.key)) continue;
+            if (x < pos) lo = u.key;
+            else if (x > pos && hi == (1 << 30)) hi = u.key;
+          }
+        }
         for (int v = 0; v < T; ++v) {
           if (colour(v) != c) continue;
           if (excluded[v]) continue;
+          if (informed && !is_joker(rules, v) && !(lo < v && v < hi)) continue;
           out.push_back(((u32)j << 24) | ((u32)pos << 16) | (u32)v);
         }
       }
@@ -367,7 +379,7 @@ void root_legal(const Obs &o, std::vector<u32> &out) {
 const u32 CRN_WORD = 0xFFFFFFFEu;
 
 int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
-            std::vector<u32> &L, bool crn = false) {
+            std::vector<u32> &L, bool crn = false, bool informed = false) {
   u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
   Block D = philox(0xFFFFFFFFu, s, crn ? CRN_WORD : code, node, k0, k1);
   u64 rho = rank64(sp.N, D.v[0], D.v[1]);
@@ -377,7 +389,7 @@ int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
   while (st != Game::FINISH) {
     Block B = philox(k, s, code, node, k0, k1);
     if (st == Game::END_TURN) G.start_turn(B.v[0], B.v[1]);
-    G.legal(L);
+    G.legal(L, informed);
     u32 n = (u32)L.size() + ((G.rules.consecutive && G.corr >= 1) ? 1u : 0u);
     u32 i = choose(n, B.v[2]);
     k += 1;
@@ -462,8 +474,9 @@ int oracle_legal(const int32_t *obs, uint32_t *codes, int32_t cap, int32_t *n_ou
 }
 
 // hist[a*P + w] += #playouts s in [s0, s1) of action a won by seat w
-int oracle_rollout_crn(const int32_t *obs, const uint32_t *codes, int32_t n_codes, uint64_t seed,
-                       uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist, int32_t crn) {
+// flags: bit 0 = common random numbers (§R3), bit 1 = informed policy (§R10)
+int oracle_rollout_flags(const int32_t *obs, const uint32_t *codes, int32_t n_codes, uint64_t seed,
+                         uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist, int32_t flags) {
   try {
     Obs o = parse(obs);
     DetSpace sp(o);
@@ -475,14 +488,15 @@ int oracle_rollout_crn(const int32_t *obs, const uint32_t *codes, int32_t n_code
     int P = o.rules.P;
     for (int a = 0; a < n_codes; ++a)
       for (u64 s = s0; s < s1; ++s)
-        hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L, crn != 0)] += 1;
+        hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L, (flags & 1) != 0,
+                                     (flags & 2) != 0)] += 1;
     return 0;
   } catch (std::exception &e) { g_err = e.what(); return -1; }
 }
 
 int oracle_rollout(const int32_t *obs, const uint32_t *codes, int32_t n_codes, uint64_t seed,
                    uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist) {
-  return oracle_rollout_crn(obs, codes, n_codes, seed, node, s0, s1, hist, 0);
+  return oracle_rollout_flags(obs, codes, n_codes, seed, node, s0, s1, hist, 0);
 }
 
 // deep-tree batch: hist[a*P + w], voids[a] for forced path + codes[a]
