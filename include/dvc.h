@@ -140,20 +140,30 @@ int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t
                             uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
                             uint64_t *d_hist, uint64_t *d_visits, int32_t device, void *cuda_stream);
 
-/* Common random numbers across actions (DESIGN.md §R3
- * "CRN"): as dvc_rollout_batch_ex / dvc_rollout_batch_async, except that the
- * determinization block of sim s is D = Philox(ctr = (0xFFFFFFFF, s,
- * 0xFFFFFFFE, node_id)) for EVERY action, so all actions of the batch play
- * against the same hidden-tile assignment for each sim index (the decision
- * blocks B_t stay keyed by the action code).  Differences between actions
- * then have lower variance; each action's counts alone have the same
- * distribution as without CRN.  hist is HOST (_ex) or DEVICE, added to (_async). */
-int dvc_rollout_batch_crn_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
-                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
-                             int32_t device);
-int dvc_rollout_batch_crn_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
-                                uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
-                                int32_t device, void *cuda_stream);
+/* Batch variants, selected by `flags` (other bits ->
+ * DVC_E_CONFIG); otherwise as dvc_rollout_batch_ex (hist HOST, overwritten)
+ * and dvc_rollout_batch_async (d_hist DEVICE, added to on cuda_stream):
+ *  DVC_FLAG_CRN       common random numbers across actions:
+ *                     the determinization block of sim s is D = Philox(ctr =
+ *                     (0xFFFFFFFF, s, 0xFFFFFFFE, node_id)) for EVERY action,
+ *                     so all actions play against the same hidden-tile
+ *                     assignment for each sim index (the decision blocks B_t
+ *                     stay keyed by the action code); each action's counts
+ *                     keep their distribution, differences get less variance.
+ *  DVC_FLAG_INFORMED  order-aware playout policy: every
+ *                     playout decision is uniform over the guesses whose value
+ *                     lies strictly between the nearest revealed numbered
+ *                     tiles left and right of the slot (joker values always
+ *                     kept), LEGAL order, STOP last.  Root actions: any LEGAL.
+ * Both flags may be combined.  Not available for deep-tree (path) batches. */
+#define DVC_FLAG_CRN 1u
+#define DVC_FLAG_INFORMED 2u
+int dvc_rollout_batch_flags_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                               uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
+                               uint64_t *hist, int32_t device);
+int dvc_rollout_batch_flags_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                                  uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
+                                  uint64_t *d_hist, int32_t device, void *cuda_stream);
 
 /* Debug/parity form of the async call: additionally writes the winner seat of
  * every playout to d_winners[a*(sim_end-sim_begin) + (s - sim_begin)] (DEVICE,
@@ -209,6 +219,8 @@ typedef struct {
   uint64_t seed;            /* Philox seed of every batch                     */
   int32_t flat;             /* 1 = root-only tree                             */
   int32_t device;           /* CUDA ordinal, -1 = current                     */
+  uint32_t flags;           /* DVC_FLAG_* for every batch (flat = 1 only)     */
+  uint32_t _pad;
 } dvc_search_params;
 typedef struct { uint32_t code, _pad; uint64_t visits, wins; } dvc_action_stat;
 int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table, int32_t cap,

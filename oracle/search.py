@@ -24,8 +24,9 @@ def best_child(stats):
     return min(stats, key=lambda t: (-t[1], -t[2], t[0]))[0]
 
 
-def flat_search(obs_json, expansions, sims_per_child, seed, c=math.sqrt(2.0)):
-    """Returns (best_code, [(code, visits, wins)] in LEGAL order)."""
+def flat_search(obs_json, expansions, sims_per_child, seed, c=math.sqrt(2.0), crn=False, informed=False):
+    """Returns (best_code, [(code, visits, wins)] in LEGAL order); crn /
+    informed select the batch variants (§R10) for every batch."""
     codes = oracle_legal(obs_json)
     viewer = obs_json["viewer"]
     visits = [0] * len(codes)
@@ -39,7 +40,8 @@ def flat_search(obs_json, expansions, sims_per_child, seed, c=math.sqrt(2.0)):
             if best is None or v > bv or (v == bv and codes[a] < codes[best]):
                 best, bv = a, v
         # SIMULATION of sims [visits, visits + n) of that child (node 0)
-        h = oracle_rollout(obs_json, [codes[best]], seed, 0, visits[best], visits[best] + sims_per_child)[0]
+        h = oracle_rollout(obs_json, [codes[best]], seed, 0, visits[best], visits[best] + sims_per_child,
+                           crn=crn, informed=informed)[0]
         # BACKPROPAGATION
         visits[best] += sims_per_child
         wins[best] += h[viewer]

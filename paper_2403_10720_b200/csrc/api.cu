@@ -18,15 +18,15 @@
 #include "rollout.cuh"
 
 namespace dvc {
-cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int grid, int block,
+cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int mode, int grid, int block,
                            size_t smem, cudaStream_t stream);
 cudaError_t launch_table(const uint8_t *plan, uint64_t N, uint4 *out, cudaStream_t stream);
 cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaStream_t stream);
-cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, bool path, int block, size_t smem,
+cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int mode, int block, size_t smem,
                              int *blocks_per_sm);
-cudaError_t search_occupancy(int P, bool jok, bool cons, int block, size_t smem, int *blocks_per_sm);
-cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, int grid,
-                               int block, size_t smem, cudaStream_t stream);
+cudaError_t search_occupancy(int P, bool jok, bool cons, bool inf, int block, size_t smem, int *blocks_per_sm);
+cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, bool inf,
+                               int grid, int block, size_t smem, cudaStream_t stream);
 
 namespace {
 
@@ -225,6 +225,7 @@ struct PathArg {
   int32_t len = 0;
   unsigned long long *d_voids = nullptr;
   bool crn = false;         // common random numbers across actions (root batches only)
+  bool informed = false;    // informed playout policy (root batches only)
 };
 
 int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed, uint32_t node_id,
@@ -274,6 +275,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
 
   const int variant = (int)g_kernel.load();
   const int block = (int)g_block.load();
+  const int mode = kp.path_len > 0 ? kModePath : (path.informed ? kModeInformed : kModePlain);
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
   size_t smem = ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
   if (variant == 0) smem += (size_t)(block / 32) * 64 * (P + 7) * sizeof(uint32_t);
@@ -283,15 +285,15 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   if (grid_opt <= 0) {
     // resident blocks per SM, cached per (kernel instance, block, smem)
     const uint64_t okey = ((uint64_t)variant << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
-                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)(kp.path_len > 0) << 53) |
+                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)mode << 51) |
                           ((uint64_t)block << 32) | (uint64_t)smem;
     int per_sm = 0;
     auto it = d->occupancy.find(okey);
     if (it != d->occupancy.end()) {
       per_sm = it->second;
     } else {
-      cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, kp.path_len > 0, block,
-                                       smem, &per_sm);
+      cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, mode, block, smem,
+                                       &per_sm);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy");
       d->occupancy[okey] = per_sm;
     }
@@ -321,7 +323,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
       const uint64_t need = ((uint64_t)kp.total + per_block - 1) / per_block;
       if (need < (uint64_t)grid) grid = (int)need;
     }
-    e = launch_rollout(kp, P, st->jokers != 0, st->consecutive != 0, variant, grid, block, smem, stream);
+    e = launch_rollout(kp, P, st->jokers != 0, st->consecutive != 0, variant, mode, grid, block, smem, stream);
     g_launches++;
     if (e != cudaSuccess) return cuda_fail(e, "rollout kernel launch");
     b = e_;
@@ -366,7 +368,10 @@ int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, c
       e = cudaMemcpyAsync(L->d_search + off_bp, batch_pos, (size_t)A * 4, cudaMemcpyHostToDevice, L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "search setup");
   }
-  int rc = enqueue(s, first, k, p->seed, 0u, 0, n, L->d_hist, nullptr, d->device, L->stream, nullptr);
+  PathArg opt;
+  opt.crn = (p->flags & DVC_FLAG_CRN) != 0;
+  opt.informed = (p->flags & DVC_FLAG_INFORMED) != 0;
+  int rc = enqueue(s, first, k, p->seed, 0u, 0, n, L->d_hist, nullptr, d->device, L->stream, nullptr, opt);
   if (rc) return rc;
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));
@@ -381,6 +386,7 @@ int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, c
     rc = get_plan(d, *st, L->stream, &plan);
     if (rc) return rc;
     fill_kparams(kp, st, p->seed, 0u, (uint32_t)A, plan, d);
+    kp.crn = opt.crn ? 1u : 0u;
     SearchArgs sa;
     sa.lnN = reinterpret_cast<const double *>(L->d_search);
     sa.delta = reinterpret_cast<unsigned long long *>(L->d_search + off_delta);
@@ -393,21 +399,22 @@ int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, c
     const int block = 128;
     const size_t smem = (size_t)A * 16;
     const uint64_t okey = (3ull << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
-                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)block << 32) | (uint64_t)smem;
+                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)opt.informed << 53) |
+                          ((uint64_t)block << 32) | (uint64_t)smem;
     int per_sm = 0;
     auto it = d->occupancy.find(okey);
     if (it != d->occupancy.end()) {
       per_sm = it->second;
     } else {
-      cudaError_t e = search_occupancy(P, st->jokers != 0, st->consecutive != 0, block, smem, &per_sm);
+      cudaError_t e = search_occupancy(P, st->jokers != 0, st->consecutive != 0, opt.informed, block, smem, &per_sm);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy");
       d->occupancy[okey] = per_sm;
     }
     if (per_sm < 1) return set_err(DVC_E_CONFIG, "search kernel cannot launch");
     uint64_t grid = (n + block - 1) / block;
     if (grid > (uint64_t)per_sm * d->num_sms) grid = (uint64_t)per_sm * d->num_sms;
-    cudaError_t e = launch_flat_search(kp, sa, P, st->jokers != 0, st->consecutive != 0, (int)grid, block, smem,
-                                       L->stream);
+    cudaError_t e = launch_flat_search(kp, sa, P, st->jokers != 0, st->consecutive != 0, opt.informed, (int)grid,
+                                       block, smem, L->stream);
     g_launches++;
     if (e != cudaSuccess) return cuda_fail(e, "flat_search_kernel launch");
     e = cudaMemcpyAsync(out.data(), sa.out, out.size() * 8, cudaMemcpyDeviceToHost, L->stream);
@@ -474,7 +481,8 @@ namespace dvc {
 namespace {
 int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                      uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist, uint64_t *visits,
-                     int32_t device, bool crn) {
+                     int32_t device, uint32_t flags) {
+  if (flags & ~(uint32_t)(DVC_FLAG_CRN | DVC_FLAG_INFORMED)) return set_err(DVC_E_CONFIG, "unknown batch flag");
   if (!hist) return set_err(DVC_E_CONFIG, "hist is null");
   const State *st = s ? as_state(s) : nullptr;
   if (!st) return set_err(DVC_E_CONFIG, "bad state");
@@ -502,7 +510,8 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
   }
   PathArg opt;
-  opt.crn = crn;
+  opt.crn = (flags & DVC_FLAG_CRN) != 0;
+  opt.informed = (flags & DVC_FLAG_INFORMED) != 0;
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
                    L->stream, nullptr, opt);
   if (rc) return rc;
@@ -519,11 +528,13 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
 
 int rollout_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                   uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist, uint64_t *d_visits,
-                  int32_t device, void *cuda_stream, bool crn) {
+                  int32_t device, void *cuda_stream, uint32_t flags) {
   if (!d_hist) return set_err(DVC_E_CONFIG, "d_hist is null");
+  if (flags & ~(uint32_t)(DVC_FLAG_CRN | DVC_FLAG_INFORMED)) return set_err(DVC_E_CONFIG, "unknown batch flag");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   PathArg opt;
-  opt.crn = crn;
+  opt.crn = (flags & DVC_FLAG_CRN) != 0;
+  opt.informed = (flags & DVC_FLAG_INFORMED) != 0;
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
                    reinterpret_cast<unsigned long long *>(d_hist), nullptr, device, stream, nullptr, opt);
   if (rc) return rc;
@@ -543,20 +554,20 @@ extern "C" {
 int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                          uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
                          uint64_t *visits, int32_t device) {
-  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, visits, device, false);
+  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, visits, device, 0u);
 }
 
-int dvc_rollout_batch_crn_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
-                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
-                             int32_t device) {
-  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, true);
+int dvc_rollout_batch_flags_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                               uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
+                               uint64_t *hist, int32_t device) {
+  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, flags);
 }
 
-int dvc_rollout_batch_crn_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
-                                uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
-                                int32_t device, void *cuda_stream) {
+int dvc_rollout_batch_flags_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
+                                  uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
+                                  uint64_t *d_hist, int32_t device, void *cuda_stream) {
   return rollout_async(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d_hist, nullptr, device,
-                       cuda_stream, true);
+                       cuda_stream, flags);
 }
 
 int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_len, const uint32_t *actions,
@@ -629,7 +640,7 @@ int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t
                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
                             uint64_t *d_visits, int32_t device, void *cuda_stream) {
   return rollout_async(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d_hist, d_visits, device,
-                       cuda_stream, false);
+                       cuda_stream, 0u);
 }
 
 int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,

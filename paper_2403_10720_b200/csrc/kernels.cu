@@ -76,9 +76,10 @@ __device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P,
 
 // Start of playout (a, s): determinization block D, table lookup (a2), root
 // action (a3).  Returns the step state.
-template <int P, bool JOK, bool CONS, bool PATH>
+template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t code, uint32_t meta,
                                                   const KParams &kp) {
+  constexpr bool PATH = MODE == kModePath;
   const uint4 D = philox_rk(0xFFFFFFFFu, s, kp.crn ? kCrnWord : code, kp.node, kp);
   determinize<P>(S, D, kp);
   uint32_t t;
@@ -90,10 +91,11 @@ __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_
 }
 
 // Decision step k of a running playout (a4), given its Philox block B_k.
-template <int P, bool JOK, bool CONS, bool PATH>
+template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint4 B, uint32_t k,
                                                const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                const KParams &kp) {
+  constexpr bool PATH = MODE == kModePath;
   turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
 #ifdef DVC_DEBUG
   dbg_check_state<P, JOK>(S, kp);
@@ -112,6 +114,8 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
     stop = forced_decide<P, JOK, CONS>(S, m, kp, &t, &correct, &illegal);
     S.fi += 1;
     if (illegal) return VOID;
+  } else if constexpr (MODE == kModeInformed) {
+    stop = decide_informed<P, JOK, CONS>(S, B.z, kp, &t, &correct);
   } else {
     stop = decide<P, JOK, CONS>(S, B.z, kp, &t, &correct);
   }
@@ -133,15 +137,16 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
 #endif
 }
 
-template <int P, bool JOK, bool CONS, bool PATH>
+template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
                                                  const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                  const KParams &kp) {
-  return step_block<P, JOK, CONS, PATH>(S, st, philox_rk(k, s, code, kp.node, kp), k, meta_of_a, path_of, a, kp);
+  return step_block<P, JOK, CONS, MODE>(S, st, philox_rk(k, s, code, kp.node, kp), k, meta_of_a, path_of, a, kp);
 }
 
-template <int P, bool JOK, bool CONS, bool PATH>
+template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_constant__ KParams kp) {
+  constexpr bool PATH = MODE == kModePath;
   const Smem sm = setup_smem(kp, P);
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kp.total; w += stride) {
@@ -149,9 +154,9 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
     const uint32_t s = kp.s0 + (w - a * kp.n_per);
     const uint32_t code = sm.codes[a], meta = sm.meta[a];
     Sim<P> S;
-    uint32_t st = start_playout<P, JOK, CONS, PATH>(S, s, code, meta, kp);
+    uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, code, meta, kp);
     for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
-      st = step_playout<P, JOK, CONS, PATH>(S, st, k, s, code, sm.meta, sm.path, a, kp);
+      st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
     record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
   flush_hist(sm.hist, kp, P);
@@ -204,8 +209,9 @@ struct RingView {
   }
 };
 
-template <int P, bool JOK, bool CONS, bool PATH>
+template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_constant__ KParams kp) {
+  constexpr bool PATH = MODE == kModePath;
   const Smem sm = setup_smem(kp, P);
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       Sim<P> T;
       uint32_t pst = FINISH;
       if (valid) {
-        pst = start_playout<P, JOK, CONS, PATH>(T, ps, pcode, pmeta, kp);
+        pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcode, pmeta, kp);
         if (pst == FINISH) {                    // decided by the root action alone
           record(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
           valid = false;
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
     }
     // ---- one decision step for every running lane
     if (active) {
-      st = step_playout<P, JOK, CONS, PATH>(S, st, k, s, code, sm.meta, sm.path, a, kp);
+      st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
       ++k;
       if (st == FINISH || st == VOID) {
         record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
@@ -328,7 +334,7 @@ __device__ __forceinline__ bool ucb_better(double v, uint32_t code, uint32_t i, 
   return v > bv || (v == bv && code < bcode);
 }
 
-template <int P, bool JOK, bool CONS>
+template <int P, bool JOK, bool CONS, bool INF>
 __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant__ KParams kp,
                                                           const __grid_constant__ SearchArgs sa) {
   namespace cg = cooperative_groups;
@@ -383,13 +389,14 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
     for (uint32_t i = gtid; i < sa.n; i += gsize) {
       const uint32_t s = sbase + i;
       Sim<P> S;
-      uint32_t st = start_playout<P, JOK, CONS, false>(S, s, code, meta, kp);
+      constexpr int MODE = INF ? kModeInformed : kModePlain;
+      uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, code, meta, kp);
       // latency-bound loop: B_{k+1} is independent of the state, so it is
       // generated while step k runs
       uint4 B = philox_rk(0u, s, code, kp.node, kp);
       for (uint32_t k = 0; st != FINISH; ++k) {
         const uint4 Bn = philox_rk(k + 1u, s, code, kp.node, kp);
-        st = step_block<P, JOK, CONS, false>(S, st, B, k, nullptr, nullptr, 0, kp);
+        st = step_block<P, JOK, CONS, MODE>(S, st, B, k, nullptr, nullptr, 0, kp);
         B = Bn;
       }
       cnt += winner_seat(S) == kp.g0 ? 1u : 0u;
@@ -412,13 +419,15 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
 }
 
 template <int P, bool JOK, bool CONS>
-const void *search_fn() { return (const void *)flat_search_kernel<P, JOK, CONS>; }
+const void *search_fn(bool inf) {
+  return inf ? (const void *)flat_search_kernel<P, JOK, CONS, true> : (const void *)flat_search_kernel<P, JOK, CONS, false>;
+}
 
-const void *select_search(int P, bool jok, bool cons) {
+const void *select_search(int P, bool jok, bool cons, bool inf) {
 #define DVC_SCASE(PP)                                                                            \
   if (P == PP) {                                                                                 \
-    if (jok) return cons ? search_fn<PP, true, true>() : search_fn<PP, true, false>();          \
-    return cons ? search_fn<PP, false, true>() : search_fn<PP, false, false>();                 \
+    if (jok) return cons ? search_fn<PP, true, true>(inf) : search_fn<PP, true, false>(inf);    \
+    return cons ? search_fn<PP, false, true>(inf) : search_fn<PP, false, false>(inf);           \
   }
   DVC_SCASE(2)
   DVC_SCASE(3)
@@ -427,15 +436,15 @@ const void *select_search(int P, bool jok, bool cons) {
   return nullptr;
 }
 
-cudaError_t search_occupancy(int P, bool jok, bool cons, int block, size_t smem, int *blocks_per_sm) {
-  const void *f = select_search(P, jok, cons);
+cudaError_t search_occupancy(int P, bool jok, bool cons, bool inf, int block, size_t smem, int *blocks_per_sm) {
+  const void *f = select_search(P, jok, cons, inf);
   if (!f) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
 }
 
-cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, int grid,
-                               int block, size_t smem, cudaStream_t stream) {
-  const void *f = select_search(P, jok, cons);
+cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, bool inf,
+                               int grid, int block, size_t smem, cudaStream_t stream) {
+  const void *f = select_search(P, jok, cons, inf);
   if (!f) return cudaErrorInvalidValue;
   void *args[] = {(void *)&kp, (void *)&sa};
   return cudaLaunchCooperativeKernel(f, grid, block, args, smem, stream);
@@ -449,18 +458,23 @@ cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaSt
 
 typedef void (*KernelFn)(const KParams);
 
-template <int P, bool JOK, bool CONS>
-KernelFn pick_kernel(int variant, bool path) {
-  if (path)
-    return variant == 1 ? rollout_naive_kernel<P, JOK, CONS, true> : rollout_refill_kernel<P, JOK, CONS, true>;
-  return variant == 1 ? rollout_naive_kernel<P, JOK, CONS, false> : rollout_refill_kernel<P, JOK, CONS, false>;
+template <int P, bool JOK, bool CONS, int MODE>
+KernelFn pick_mode(int variant) {
+  return variant == 1 ? rollout_naive_kernel<P, JOK, CONS, MODE> : rollout_refill_kernel<P, JOK, CONS, MODE>;
 }
 
-KernelFn select_kernel(int P, bool jok, bool cons, int variant, bool path) {
+template <int P, bool JOK, bool CONS>
+KernelFn pick_kernel(int variant, int mode) {
+  if (mode == kModePath) return pick_mode<P, JOK, CONS, kModePath>(variant);
+  if (mode == kModeInformed) return pick_mode<P, JOK, CONS, kModeInformed>(variant);
+  return pick_mode<P, JOK, CONS, kModePlain>(variant);
+}
+
+KernelFn select_kernel(int P, bool jok, bool cons, int variant, int mode) {
 #define DVC_CASE(PP)                                                                                 \
   if (P == PP) {                                                                                     \
-    if (jok) return cons ? pick_kernel<PP, true, true>(variant, path) : pick_kernel<PP, true, false>(variant, path); \
-    return cons ? pick_kernel<PP, false, true>(variant, path) : pick_kernel<PP, false, false>(variant, path);       \
+    if (jok) return cons ? pick_kernel<PP, true, true>(variant, mode) : pick_kernel<PP, true, false>(variant, mode); \
+    return cons ? pick_kernel<PP, false, true>(variant, mode) : pick_kernel<PP, false, false>(variant, mode);       \
   }
   DVC_CASE(2)
   DVC_CASE(3)
@@ -469,16 +483,16 @@ KernelFn select_kernel(int P, bool jok, bool cons, int variant, bool path) {
   return nullptr;
 }
 
-cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, bool path, int block, size_t smem,
+cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int mode, int block, size_t smem,
                              int *blocks_per_sm) {
-  KernelFn f = select_kernel(P, jok, cons, variant, path);
+  KernelFn f = select_kernel(P, jok, cons, variant, mode);
   if (!f) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (const void *)f, block, smem);
 }
 
-cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int grid, int block,
+cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int mode, int grid, int block,
                            size_t smem, cudaStream_t stream) {
-  KernelFn f = select_kernel(P, jok, cons, variant, kp.path_len > 0);
+  KernelFn f = select_kernel(P, jok, cons, variant, mode);
   if (!f) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -149,6 +149,9 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
   if (st->magic != kMagic) return set_error(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
   if (p->expansions < 1 || p->sims_per_child < 1 || !(p->c >= 0.0))
     return set_error(DVC_E_CONFIG, "need expansions >= 1, sims_per_child >= 1, c >= 0");
+  if (p->flags & ~(uint32_t)(DVC_FLAG_CRN | DVC_FLAG_INFORMED))
+    return set_error(DVC_E_CONFIG, "unknown search flag");
+  if (p->flags && !p->flat) return set_error(DVC_E_CONFIG, "batch flags need flat = 1 (no path batches)");
   int32_t A = 0;
   legal_actions(*st, nullptr, 0, &A);
   *n_out = A;
@@ -190,7 +193,7 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
       return finish(codes, visits, wins, table, best_code);
     }
     std::vector<uint64_t> h((size_t)k * st->P);
-    int rc = dvc_rollout_batch_ex(s, first.data(), k, p->seed, 0u, 0, n, h.data(), nullptr, p->device);
+    int rc = dvc_rollout_batch_flags_ex(s, first.data(), k, p->seed, 0u, 0, n, p->flags, h.data(), p->device);
     if (rc) return rc;
     for (int i = 0; i < k; ++i) {
       visits[order[i]] = n;
@@ -215,8 +218,8 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     if (visits[best] + n > (1ull << 32))
       return set_error(DVC_E_CONFIG, "a child's sim index range would pass 2^32");
     // simulation on the GPU: sims [visits, visits + n) of the chosen child
-    int rc = dvc_rollout_batch_ex(s, &codes[best], 1, p->seed, 0u, visits[best], visits[best] + n, hist.data(),
-                                  nullptr, p->device);
+    int rc = dvc_rollout_batch_flags_ex(s, &codes[best], 1, p->seed, 0u, visits[best], visits[best] + n, p->flags,
+                                        hist.data(), p->device);
     if (rc) return rc;
     // backpropagation
     visits[best] += n;

@@ -17,7 +17,9 @@ namespace dvc {
 constexpr int kMaxActions = 768;
 
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
-constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's counter word z under common random numbers (no action code)
+constexpr uint32_t kCrnWord = 0xFFFFFFFEu;
+// Kernel modes: root batches, deep-tree (forced path) batches, informed policy (§R10).
+constexpr int kModePlain = 0, kModePath = 1, kModeInformed = 2;   // D's counter word z under common random numbers (no action code)
 
 struct KParams {
   uint32_t k0, k1;        // Philox key = (lo32(seed), hi32(seed))
@@ -383,6 +385,144 @@ __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t wz, const KPara
   *t_out = t;
   *correct = vidx == (uint32_t)__popc(((t & 1u) ? aW : aB) & below(t));
   return stop;
+}
+
+// ----------------------------------------------------------------- informed policy (§R10)
+// Numbered keys strictly between the nearest revealed numbered keys of a line
+// (Rd) below `pivot` and at/above it: the candidate window of a hidden slot
+// whose true key is pivot (numbered slot) or whose joker threshold is pivot.
+__device__ __forceinline__ uint32_t bound_mask(uint32_t Rd, uint32_t pivot) {
+  const uint32_t lo = Rd & below(pivot), hi = Rd & ~below(pivot);
+  const uint32_t upper = hi ? below(__ffs(hi) - 1u) : 0xFFFFFFFFu;
+  const uint32_t lower = lo ? ~below(32u - __clz(lo)) : 0xFFFFFFFFu;
+  return upper & lower;
+}
+
+// Candidates of one slot: numbered values of its colour inside the window,
+// then the joker of that colour when available.
+struct InfCtx {
+  uint32_t num[2];   // available numbered values per colour
+  uint32_t jav[2];   // joker of that colour available (0/1)
+};
+
+__device__ __forceinline__ uint32_t slot_weight(const InfCtx &c, uint32_t Rd, uint32_t pivot, uint32_t col) {
+  return (uint32_t)__popc(c.num[col] & bound_mask(Rd, pivot)) + c.jav[col];
+}
+
+// Total weight of the hidden slots of hand Hd (any order).
+template <bool JOK>
+__device__ __forceinline__ uint32_t informed_total(const InfCtx &c, uint32_t Hd, uint32_t V, uint32_t ji,
+                                                   const KParams &kp) {
+  const uint32_t hid = Hd & ~V, Rd = Hd & V & kp.numm;
+  uint32_t tot = 0;
+  for (uint32_t m = hid & kp.numm; m; m &= m - 1u) {
+    const uint32_t t = __ffs(m) - 1u;
+    tot += slot_weight(c, Rd, t, t & 1u);
+  }
+  if (JOK) {
+    if ((hid >> kp.JB) & 1u) tot += slot_weight(c, Rd, kap_b(ji), 0u);
+    if ((hid >> (kp.JB + 1)) & 1u) tot += slot_weight(c, Rd, kap_w(ji), 1u);
+  }
+  return tot;
+}
+
+// Walk the hidden slots of Hd in LINE order (numbered keys ascending, a joker
+// before the numbered keys >= its threshold, JW before JB in one gap iff bit 10)
+// and return the slot holding index x plus the value index inside it.
+template <bool JOK>
+__device__ __forceinline__ void informed_select(const InfCtx &c, uint32_t Hd, uint32_t V, uint32_t ji, uint32_t x,
+                                                const KParams &kp, uint32_t *t_out, uint32_t *vidx_out,
+                                                uint32_t *win_out) {
+  const uint32_t hid = Hd & ~V, Rd = Hd & V & kp.numm;
+  // joker slots as sort keys 4*kappa + order (numbered key t sorts at 4t + 3)
+  // (jk0, jt0) is the next joker slot, (jk1, jt1) the one after it
+  uint32_t jk0 = 0xFFFFFFFFu, jt0 = 0, jk1 = 0xFFFFFFFFu, jt1 = 0;
+  if (JOK) {
+    const bool hb = (hid >> kp.JB) & 1u, hw = (hid >> (kp.JB + 1)) & 1u;
+    const bool wfirst = (ji >> 10) & 1u;
+    const uint32_t kb = 4u * kap_b(ji) + (wfirst ? 1u : 0u), kw = 4u * kap_w(ji) + (wfirst ? 0u : 1u);
+    if (hb && hw) {
+      const bool bfirst = kb < kw;
+      jk0 = bfirst ? kb : kw; jt0 = bfirst ? kp.JB : kp.JB + 1u;
+      jk1 = bfirst ? kw : kb; jt1 = bfirst ? kp.JB + 1u : kp.JB;
+    } else if (hb) {
+      jk0 = kb; jt0 = kp.JB;
+    } else if (hw) {
+      jk0 = kw; jt0 = kp.JB + 1u;
+    }
+  }
+  uint32_t acc = 0;
+  uint32_t m = hid & kp.numm;
+  while (true) {
+    const uint32_t tn = m ? __ffs(m) - 1u : 0xFFFFFFFFu;
+    const uint32_t nkey = m ? 4u * tn + 3u : 0xFFFFFFFFu;
+    const bool take_joker = JOK && jk0 < nkey;
+    if (!take_joker && !m) break;                       // cannot happen: x < total
+    const uint32_t t = take_joker ? jt0 : tn;
+    const uint32_t col = take_joker ? t - kp.JB : (t & 1u);
+    const uint32_t pivot = take_joker ? (jk0 >> 2) : t;
+    const uint32_t win = c.num[col] & bound_mask(Rd, pivot);
+    const uint32_t w = (uint32_t)__popc(win) + c.jav[col];
+    if (x < acc + w) {
+      *t_out = t;
+      *vidx_out = x - acc;
+      *win_out = win;
+      return;
+    }
+    acc += w;
+    if (take_joker) {
+      jk0 = jk1; jt0 = jt1; jk1 = 0xFFFFFFFFu;
+    } else {
+      m &= m - 1u;
+    }
+  }
+  *t_out = kNoKey;
+  *vidx_out = 0;
+  *win_out = 0;
+}
+
+// One informed decision: as decide(), over the order-aware list.
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t wz, const KParams &kp, uint32_t *t_out,
+                                                bool *correct) {
+  const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
+  InfCtx c;
+  c.num[0] = avail & kp.numm & kEven;
+  c.num[1] = avail & kp.numm & kOdd;
+  c.jav[0] = JOK ? (avail >> kp.JB) & 1u : 0u;
+  c.jav[1] = JOK ? (avail >> (kp.JB + 1)) & 1u : 0u;
+  uint32_t cnt[P];
+  uint32_t tot = 0;
+#pragma unroll
+  for (int d = 1; d < P; ++d) {
+    cnt[d] = informed_total<JOK>(c, S.H[d], S.V, S.ji, kp);
+    tot += cnt[d];
+  }
+  const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
+  uint32_t x = choose(n, wz);
+  const bool stop = CONS && x >= tot;
+  uint32_t d = 1;
+  if (P > 2) {
+    bool found = false;
+#pragma unroll
+    for (int dd = 1; dd < P; ++dd) {
+      const bool here = !found && x < cnt[dd];
+      d = here ? (uint32_t)dd : d;
+      x = (!found && !here) ? x - cnt[dd] : x;
+      found = found || here;
+    }
+  }
+  if (stop) {
+    *t_out = kNoKey;
+    *correct = false;
+    return true;
+  }
+  uint32_t t, vidx, win;
+  informed_select<JOK>(c, pick<P>(S.H, d), S.V, S.ji, x, kp, &t, &vidx, &win);
+  *t_out = t;
+  // the slot's list: numbered values of the window ascending, then the joker
+  *correct = (JOK && t >= kp.JB) ? vidx == (uint32_t)__popc(win) : vidx == (uint32_t)__popc(win & below(t));
+  return false;
 }
 
 // ----------------------------------------------------------------- determinization (§R4)

@@ -26,7 +26,7 @@ HIDDEN = 0xFF
 # every symbol include/dvc.h declares
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
            "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async",
-           "dvc_rollout_batch_crn_ex", "dvc_rollout_batch_crn_async", "dvc_mcts_search",
+           "dvc_rollout_batch_flags_ex", "dvc_rollout_batch_flags_async", "dvc_mcts_search",
            "dvc_set_option", "dvc_get_option", "dvc_debug_counters", "dvc_launch_count", "dvc_last_error",
            "dvc_shutdown"]
 
@@ -60,7 +60,7 @@ class _State(ctypes.Structure):
 class _SearchParams(ctypes.Structure):
     _fields_ = [("c", ctypes.c_double), ("max_depth", ctypes.c_int32), ("expansions", ctypes.c_int32),
                 ("sims_per_child", ctypes.c_uint64), ("seed", ctypes.c_uint64), ("flat", ctypes.c_int32),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("flags", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
 
 
 class _ActionStat(ctypes.Structure):
@@ -98,8 +98,8 @@ def lib():
                                           I32]
         L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
-        L.dvc_rollout_batch_crn_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, P(U64), I32]
-        L.dvc_rollout_batch_crn_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, I32, VP]
+        L.dvc_rollout_batch_flags_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, U32, P(U64), I32]
+        L.dvc_rollout_batch_flags_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, U32, VP, I32, VP]
         L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
         L.dvc_debug_counters.argtypes = [I32, P(U32)]
         L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
@@ -203,16 +203,25 @@ def rollout_batch(state, actions, n_sims, seed):
     return wins
 
 
-def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-1, crn=False):
+FLAG_CRN, FLAG_INFORMED = 1, 2
+
+
+def _flags(crn, informed):
+    return (FLAG_CRN if crn else 0) | (FLAG_INFORMED if informed else 0)
+
+
+def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-1, crn=False, informed=False):
     """hist[a, w] (numpy uint64, host) for sims [sim_begin, sim_end) (blocking).
-    crn: common determinizations across actions (dvc_rollout_batch_crn_ex)."""
+    crn: common determinizations across actions; informed: order-aware playout
+    policy (dvc_rollout_batch_flags_ex)."""
     a, ap = _codes(actions)
     P = state.players
     hist = np.zeros((len(a), P), dtype=np.uint64)
     hp = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
-    if crn:
-        _check(lib().dvc_rollout_batch_crn_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
-                                              hp, device))
+    flags = _flags(crn, informed)
+    if flags:
+        _check(lib().dvc_rollout_batch_flags_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin,
+                                                sim_end, flags, hp, device))
     else:
         _check(lib().dvc_rollout_batch_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                           hp, None, device))
@@ -240,18 +249,20 @@ def _stream_ptr(stream):
 
 
 def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist, visits=None, stream=None,
-                        crn=False):
+                        crn=False, informed=False):
     """ADD counts into device tensors hist[A, P] (torch.int64, CUDA) and
     visits[A] (optional) on `stream` (default: torch's current stream).
-    crn: common determinizations across actions (dvc_rollout_batch_crn_async;
-    visits must then be None)."""
+    crn / informed: batch variants (dvc_rollout_batch_flags_async; visits
+    must then be None)."""
     a, ap = _codes(actions)
     dev = hist.device.index
-    if crn:
+    flags = _flags(crn, informed)
+    if flags:
         if visits is not None:
-            raise ValueError("the CRN entry point takes no visits array")
-        _check(lib().dvc_rollout_batch_crn_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin,
-                                                 sim_end, ctypes.c_void_p(hist.data_ptr()), dev, _stream_ptr(stream)))
+            raise ValueError("the flags entry point takes no visits array")
+        _check(lib().dvc_rollout_batch_flags_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin,
+                                                   sim_end, flags, ctypes.c_void_p(hist.data_ptr()), dev,
+                                                   _stream_ptr(stream)))
         return
     _check(lib().dvc_rollout_batch_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                          ctypes.c_void_p(hist.data_ptr()),
@@ -269,11 +280,13 @@ def rollout_trace_async(state, actions, seed, node_id, sim_begin, sim_end, hist,
                                          dev, _stream_ptr(stream)))
 
 
-def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, max_depth=4, flat=1, device=-1):
+def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, max_depth=4, flat=1, device=-1, crn=False,
+                informed=False):
     """Host UCT over GPU rollout batches (dvc_mcts_search).  Returns
-    (best_code, [(code, visits, wins)] in LEGAL order)."""
+    (best_code, [(code, visits, wins)] in LEGAL order).  crn / informed:
+    batch variants for every playout batch (flat = 1 only)."""
     p = _SearchParams(c=c, max_depth=max_depth, expansions=expansions, sims_per_child=sims_per_child,
-                      seed=seed, flat=flat, device=device)
+                      seed=seed, flat=flat, device=device, flags=_flags(crn, informed))
     n = ctypes.c_int32()
     best = ctypes.c_uint32()
     cap = max(1, state.info["n_legal"])

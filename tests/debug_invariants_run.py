@@ -1,5 +1,5 @@
 """Runs under DVC_DEBUG=1 (libdvc_debug.so): every committed fixture through
-both kernels (and deep-tree path batches), then prints the device-side
+both kernels (plain, deep-tree path and informed/CRN batches), then prints the device-side
 invariant counters as JSON.  Driven by tests/test_gpu_debug.py."""
 import glob
 import json
@@ -24,6 +24,7 @@ def main():
                 dvc.rollout_batch_ex(st, codes, 31, 0, 0, n)
                 guesses = [c for c in codes if c != 0xFFFFFFFF]
                 dvc.rollout_path_ex(st, [guesses[0]], codes[:8], 31, 1, 0, n // 10)
+                dvc.rollout_batch_ex(st, codes, 32, 0, 0, n // 4, crn=True, informed=True)
     print(json.dumps({"counters": list(dvc.debug_counters())}))
 
 

@@ -245,3 +245,57 @@ def test_crn_e2_complementary_at_full_size(dvc):
     h = dvc.rollout_batch_ex(st, codes, 5, 0, 0, 1000000, crn=True).astype(np.int64)
     assert int(h[0, 0] + h[1, 0]) == 1000000
     assert abs(int(h[0, 0]) - 500000) < 5 * 500                       # p = 1/2, 5 sigma
+
+
+# ---- informed (order-aware) playout policy
+INF_CASES = ["tests/golden/I1.json", "tests/golden/T1.json", "tests/golden/J1.json", "tests/golden/T2c1.json",
+             "fixtures/c1_d3.json", "fixtures/c2_d1.json", "fixtures/c3_d1.json", "fixtures/c3_d4.json",
+             "fixtures/x3_d1.json", "fixtures/x4mid_d2.json", "fixtures/c4_d1.json", "fixtures/xlate_d1.json",
+             "fixtures/xstop_d1.json", "fixtures/xc0_d2.json", "fixtures/x3nj_d1.json", "fixtures/x4jc0_d1.json"]
+
+
+@pytest.mark.parametrize("kernel", [0, 1], ids=["refill", "naive"])
+@pytest.mark.parametrize("path", INF_CASES, ids=[os.path.basename(p) for p in INF_CASES])
+def test_informed_equals_oracle(dvc, oracle_lib, path, kernel):
+    d = load(os.path.join(ROOT, path))
+    st = dvc.encode(d)
+    codes = st.legal_actions()
+    codes = codes[:6] + codes[-3:] if len(codes) > 9 else codes
+    n = 500 if d["rules"]["players"] < 4 else 150
+    for crn in (False, True):
+        exp = oracle_lib.rollout(d, codes, 8, 1, 3, 3 + n, crn=crn, informed=True)
+        with dvc.options(kernel=kernel):
+            got = dvc.rollout_batch_ex(st, codes, 8, 1, 3, 3 + n, crn=crn, informed=True).astype(np.int64).tolist()
+            hist = torch.zeros((len(codes), st.players), dtype=torch.int64, device="cuda")
+            dvc.rollout_batch_async(st, codes, 8, 1, 3, 3 + n, hist, crn=crn, informed=True)
+            torch.cuda.synchronize()
+        assert got == exp, (path, crn)
+        assert hist.cpu().tolist() == exp
+
+
+def test_informed_i1_exact_at_full_size(dvc):
+    """I1 (hand-derived, tests/golden/I1.json): under the informed policy the
+    two wrong root guesses lose every playout and the right one wins every
+    playout -- at 10^6 sims per action; the plain policy gives 1/4."""
+    d = load(os.path.join(ROOT, "tests", "golden", "I1.json"))
+    st = dvc.encode(d)
+    codes = st.legal_actions()
+    n = 1000000
+    h = dvc.rollout_batch_ex(st, codes, 4, 0, 0, n, informed=True).astype(np.int64)
+    assert h[:, 0].tolist() == [n, 0, 0]
+    hp = dvc.rollout_batch_ex(st, codes, 4, 0, 0, n).astype(np.int64)
+    for w in hp[1:, 0]:
+        assert abs(w / n - 0.25) <= 5 * (0.25 * 0.75 / n) ** 0.5
+
+
+def test_flags_errors(dvc):
+    d = load(os.path.join(ROOT, "fixtures", "c2_d1.json"))
+    st = dvc.encode(d)
+    codes = st.legal_actions()[:2]
+    import ctypes
+    L = dvc.lib()
+    a = (ctypes.c_uint32 * 2)(*codes)
+    h = (ctypes.c_uint64 * (2 * st.players))()
+    assert L.dvc_rollout_batch_flags_ex(ctypes.byref(st._s), a, 2, 1, 0, 0, 10, 4, h, -1) == -1   # unknown flag
+    with pytest.raises(dvc.DvcError):
+        dvc.mcts_search(st, 4, 10, 1, flat=0, informed=True)                   # no path batches with flags

@@ -140,3 +140,20 @@ def test_concurrent_selfplay_equals_sequential(dvc):
     kw = dict(expansions=6, sims_per_child=64, flat=0, max_depth=3)
     seq = [play_game(s, **kw) for s in seeds[:3]]
     assert play_games(seeds[:3], threads=3, **kw) == seq
+
+
+@pytest.mark.parametrize("sdev", [0, 1], ids=["host_loop", "device_loop"])
+@pytest.mark.parametrize("path", ["fixtures/c3_d2.json", "fixtures/c2_d1.json", "fixtures/x4mid_d1.json"])
+def test_flat_search_flags_equal_oracle(dvc, oracle_lib, path, sdev):
+    """Flat search with the informed policy and CRN batches (DESIGN.md §R10,
+    §R3) == the oracle's flat_search with the same flags, host and device loops."""
+    from oracle.search import flat_search
+    d = json.load(open(os.path.join(ROOT, path)))
+    st = dvc.encode(d)
+    A = len(st.legal_actions())
+    exp_n, n = A + 30, 200
+    for crn, informed in ((False, True), (True, True), (True, False)):
+        best_o, stats_o = flat_search(d, exp_n, n, 5, crn=crn, informed=informed)
+        with dvc.options(search_device=sdev):
+            best_g, stats_g = dvc.mcts_search(st, exp_n, n, 5, crn=crn, informed=informed)
+        assert [tuple(map(int, t)) for t in stats_g] == stats_o and best_g == best_o, (crn, informed)
