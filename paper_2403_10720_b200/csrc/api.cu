@@ -57,6 +57,7 @@ constexpr size_t kPlanCacheMax = 16;
 struct HostLane {
   cudaStream_t stream = nullptr;
   unsigned long long *d_hist = nullptr;
+  unsigned long long *h_hist = nullptr;  // pinned staging for the blocking calls' read-back
   size_t hist_cap = 0;
   unsigned char *d_search = nullptr;     // device flat search: lnN, delta, out, batch_pos
   size_t search_cap = 0;
@@ -97,7 +98,10 @@ int get_scratch(int device, DeviceScratch **out) {
   d->device = device;
   e = cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaDeviceGetAttribute"); }
-  e = cudaMalloc(&d->d_counters, kCounterSlots * sizeof(uint32_t));
+  // slot i = (work counter, exit count) at d_counters[2i]; zero once here, the
+  // refill kernel re-arms its slot on exit (kernels.cu)
+  e = cudaMalloc(&d->d_counters, 2 * kCounterSlots * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(d->d_counters, 0, 2 * kCounterSlots * sizeof(uint32_t));
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaMalloc(counters)"); }
 #ifdef DVC_DEBUG
   e = cudaMalloc(&d->d_debug, 4 * sizeof(uint32_t));
@@ -119,9 +123,12 @@ int get_lane(DeviceScratch *d, size_t n, HostLane **out) {
   }
   if (L.hist_cap < n) {
     if (L.d_hist) cudaFree(L.d_hist);
+    if (L.h_hist) cudaFreeHost(L.h_hist);
     L.d_hist = nullptr;
+    L.h_hist = nullptr;
     L.hist_cap = 0;
     cudaError_t e = cudaMalloc(&L.d_hist, n * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&L.h_hist, n * sizeof(unsigned long long));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(hist)");
     L.hist_cap = n;
   }
@@ -182,6 +189,9 @@ int get_plan(DeviceScratch *d, const State &st, cudaStream_t stream, PlanEntry *
   if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaEventRecord"); }
   d->plans.push_front(std::move(p));
   while (d->plans.size() > kPlanCacheMax) {
+    // kernels on other host threads' streams may still read the evicted
+    // plan/table: drain the device before freeing (rare: > 16 live states)
+    cudaDeviceSynchronize();
     free_plan(d->plans.back());
     d->plans.pop_back();
   }
@@ -312,9 +322,8 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     // ceil(2^64 / n_per) for the kernels' division-free item -> (action, sim)
     kp.div_magic = kp.n_per == 1 ? 0ull
                  : (uint64_t)(((unsigned __int128)1 << 64) / kp.n_per) + ((((unsigned __int128)1 << 64) % kp.n_per) ? 1 : 0);
-    kp.counter = d->d_counters + (d->next_counter++ % kCounterSlots);
-    cudaError_t e = cudaMemsetAsync(kp.counter, 0, sizeof(uint32_t), stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counter)");
+    kp.counter = d->d_counters + 2 * (d->next_counter++ % kCounterSlots);
+    cudaError_t e;
     // auto grid: the resident maximum, or fewer blocks for a small launch (each
     // refill warp starts 32 playouts at a time; each naive thread plays one)
     int grid = grid_full;
@@ -515,12 +524,11 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
                    L->stream, nullptr, opt);
   if (rc) return rc;
-  std::vector<unsigned long long> tmp(n);
-  cudaError_t e = cudaMemcpyAsync(tmp.data(), L->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  cudaError_t e = cudaMemcpyAsync(L->h_hist, L->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                   L->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rollout");
-  for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
+  for (size_t i = 0; i < n; ++i) hist[i] = L->h_hist[i];
   if (visits)
     for (int a = 0; a < n_actions; ++a) visits[a] = sim_end - sim_begin;
   return DVC_OK;
@@ -612,14 +620,13 @@ int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_l
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
                    L->stream, nullptr, pa);
   if (rc) return rc;
-  std::vector<unsigned long long> tmp(n + n_actions);
-  cudaError_t e = cudaMemcpyAsync(tmp.data(), L->d_hist, tmp.size() * sizeof(unsigned long long),
+  cudaError_t e = cudaMemcpyAsync(L->h_hist, L->d_hist, (n + n_actions) * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, L->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rollout");
-  for (size_t i = 0; i < n; ++i) hist[i] = tmp[i];
+  for (size_t i = 0; i < n; ++i) hist[i] = L->h_hist[i];
   if (voids)
-    for (int a = 0; a < n_actions; ++a) voids[a] = tmp[n + a];
+    for (int a = 0; a < n_actions; ++a) voids[a] = L->h_hist[n + a];
   return DVC_OK;
 }
 
@@ -731,6 +738,7 @@ void dvc_shutdown(void) {
     if (d->d_counters) cudaFree(d->d_counters);
     for (auto &kv2 : d->lanes) {
       if (kv2.second.d_hist) cudaFree(kv2.second.d_hist);
+      if (kv2.second.h_hist) cudaFreeHost(kv2.second.h_hist);
       if (kv2.second.d_search) cudaFree(kv2.second.d_search);
       if (kv2.second.stream) cudaStreamDestroy(kv2.second.stream);
     }

@@ -306,6 +306,16 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
     }
   }
   flush_hist(sm.hist, kp, P);
+  // The last block out re-arms the work counter (counter[0]) and its exit
+  // count (counter[1]) for the launch that reuses this slot, so no launch
+  // needs a memset first.  Every block stopped claiming before it counts out.
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(kp.counter + 1, 1u) == gridDim.x - 1u) {
+      atomicExch(kp.counter, 0u);
+      atomicExch(kp.counter + 1, 0u);
+    }
+  }
 }
 
 __global__ void det_table_kernel(const uint8_t *__restrict__ plan, uint64_t N, uint4 *__restrict__ out) {

@@ -13,8 +13,10 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# DVC_DEBUG=1 selects the debug build (device-side invariant checks)
-LIB_PATH = os.path.join(HERE, "libdvc_debug.so" if os.environ.get("DVC_DEBUG") == "1" else "libdvc.so")
+# DVC_DEBUG=1 selects the debug build (device-side invariant checks);
+# DVC_LIB=<file name in this directory> selects another build (A/B timing)
+LIB_PATH = os.path.join(HERE, os.environ.get("DVC_LIB") or
+                        ("libdvc_debug.so" if os.environ.get("DVC_DEBUG") == "1" else "libdvc.so"))
 
 DVC_OK = 0
 ERRORS = {-1: "DVC_E_CONFIG", -2: "DVC_E_PROTOCOL", -3: "DVC_E_ILLEGAL",
