@@ -11,11 +11,36 @@ import math
 from . import rollout as oracle_rollout, legal as oracle_legal
 
 
+LN2 = 0.6931471805599453        # the double nearest ln 2
+
+
+def ln_series(N):
+    """ln N for an integer N >= 1 by a fixed IEEE-double recipe (DESIGN.md §R8,
+    reading #28) that the C++ host tree and the CUDA search kernels evaluate
+    operation for operation, so all three choose the same UCB1 child:
+    N = m 2^e with m in [sqrt(1/2), sqrt(2)), ln N = 2 atanh(z) + e ln2 with
+    z = (m - 1)/(m + 1) (|z| < 0.172) and atanh(z) = sum_{k<14} z^(2k+1)/(2k+1),
+    summed in increasing k.  Accurate to ~1.5 ulp (tests/test_oracle_search.py)."""
+    m, e = math.frexp(float(N))
+    if m < 0.7071067811865476:
+        m *= 2.0
+        e -= 1
+    z = (m - 1.0) / (m + 1.0)
+    z2 = z * z
+    s = 0.0
+    t = z
+    for k in range(14):
+        s += t / (2 * k + 1)
+        t *= z2
+    return 2.0 * s + e * LN2
+
+
 def ucb1(wins, visits, parent_visits, c):
-    """wins/visits + c*sqrt(ln(parent)/visits); unvisited -> +inf (SPEC:243)."""
+    """wins/visits + c*sqrt(ln(parent)/visits); unvisited -> +inf (SPEC:243).
+    ln is ln_series (reading #28), evaluated in this order, no fused ops."""
     if visits == 0:
         return math.inf
-    return wins / visits + c * math.sqrt(math.log(parent_visits) / visits)
+    return wins / visits + c * math.sqrt(ln_series(parent_visits) / visits)
 
 
 def best_child(stats):

@@ -43,7 +43,7 @@ def build(force=False, verbose=False, debug=False):
         return out
     tmp = out + ".tmp.%d" % os.getpid()
     cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-O2", "-I", os.path.join(HERE, "..", "include"), "-o", tmp]
+           "-Xcompiler", "-O2", "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(HERE, "..", "include"), "-o", tmp]
     if debug:
         cmd += ["-DDVC_DEBUG"]
     if verbose:

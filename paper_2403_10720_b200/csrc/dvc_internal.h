@@ -78,6 +78,8 @@ __host__ __device__ inline uint32_t act_meta(uint32_t d, uint32_t pos, uint32_t 
 
 // ---- error reporting (api.cu): sets dvc_last_error(), returns code ----
 int set_error(int code, const char *msg);
+// ln N for UCB1 (mcts.cpp; DESIGN.md §R8 reading #28).
+double ln_series(uint64_t N);
 // Device flat search (api.cu): option "search_device", and the call itself.
 bool search_on_device();
 int flat_search_gpu(const dvc_state *s, const uint32_t *codes, int32_t A, const uint32_t *first, int32_t k,

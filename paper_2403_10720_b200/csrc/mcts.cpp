@@ -33,8 +33,35 @@ struct Node {
   std::vector<int32_t> children;
 };
 
+}  // namespace
+
+namespace dvc {
+// ln N by the fixed recipe of DESIGN.md §R8 reading #28 (the oracle's
+// ln_series, the device's ln_series_dev): the host, the oracle and the search
+// kernels evaluate the same IEEE operations in the same order (this file is
+// compiled with -ffp-contract=off), so their UCB1 choices agree bit for bit.
+double ln_series(uint64_t N) {
+  int e = 0;
+  double m = std::frexp((double)N, &e);
+  if (m < 0.7071067811865476) {
+    m *= 2.0;
+    e -= 1;
+  }
+  const double z = (m - 1.0) / (m + 1.0);
+  const double z2 = z * z;
+  double s = 0.0, t = z;
+  for (int k = 0; k < 14; ++k) {
+    s += t / (double)(2 * k + 1);
+    t *= z2;
+  }
+  return 2.0 * s + (double)e * 0.6931471805599453;
+}
+}  // namespace dvc
+
+namespace {
+
 double ucb1(uint64_t w, uint64_t v, uint64_t parent, double c) {
-  return (double)w / (double)v + c * std::sqrt(std::log((double)parent) / (double)v);
+  return (double)w / (double)v + c * std::sqrt(dvc::ln_series(parent) / (double)v);
 }
 
 int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p, std::vector<uint32_t> &root_codes,
@@ -182,11 +209,11 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     if (iters > 0 && search_on_device() && n * (uint64_t)(iters + 1) <= (1ull << 32)) {
       // The whole search on the GPU (api.cu flat_search_gpu): the same
       // selections and playouts as the host loop below, without a host round
-      // trip per iteration.  ln(N) comes from this host's libm, N = (k + it) n.
+      // trip per iteration.  ln(N) = ln_series((k + it) n), N known in advance.
       std::vector<int32_t> batch_pos((size_t)A, -1);
       for (int i = 0; i < k; ++i) batch_pos[order[i]] = i;
       std::vector<double> lnN((size_t)iters);
-      for (int i = 0; i < iters; ++i) lnN[i] = std::log((double)((uint64_t)(k + i) * n));
+      for (int i = 0; i < iters; ++i) lnN[i] = ln_series((uint64_t)(k + i) * n);
       int rc = flat_search_gpu(s, codes.data(), A, first.data(), k, batch_pos.data(), lnN.data(), iters, p,
                                visits.data(), wins.data());
       if (rc) return rc;
@@ -211,7 +238,7 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
       if (visits[a] == 0) {
         v = INFINITY;
       } else {
-        v = (double)wins[a] / (double)visits[a] + p->c * std::sqrt(std::log((double)N) / (double)visits[a]);
+        v = ucb1(wins[a], visits[a], N, p->c);
       }
       if (best < 0 || v > best_v || (v == best_v && codes[a] < codes[best])) { best = a; best_v = v; }
     }

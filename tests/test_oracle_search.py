@@ -65,3 +65,27 @@ def test_deep_search_finds_exact_best(oracle_lib):
     d = json.load(open(os.path.join(GOLD, "E1.json")))
     best, stats = deep_search(d, 4, 100, 3)
     assert stats[0][1] == stats[0][2] > 0                    # forced win, no voids at depth 1
+
+
+def test_ln_series_accuracy_and_special_values():
+    """ln_series (DESIGN.md §R8 reading #28) against a 50-digit decimal ln:
+    within 2 ulp everywhere sampled; exact 0 at N = 1; k*ln2 at N = 2^k;
+    increasing on 1..10^5."""
+    import math
+    import random
+    from decimal import Decimal, getcontext
+    from oracle.search import ln_series, LN2
+    getcontext().prec = 50
+    assert ln_series(1) == 0.0
+    for k in range(1, 63):
+        assert ln_series(1 << k) == k * LN2
+    rng = random.Random(3)
+    for N in list(range(2, 2000)) + [rng.randrange(2, 1 << 52) for _ in range(5000)]:
+        a = ln_series(N)
+        ref = Decimal(N).ln()
+        assert abs(Decimal(a) - ref) <= 2 * Decimal(math.ulp(float(ref))), N
+    prev = -1.0
+    for N in range(1, 100001):
+        v = ln_series(N)
+        assert v > prev
+        prev = v
