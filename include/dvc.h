@@ -186,10 +186,12 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
  *                0 = re-upload the plan and rebuild the table on every call
  *  "search_device" 0 = dvc_mcts_search keeps UCT selection and backprop on
  *                the host tree, one blocking rollout batch per iteration
- *                (default; BASELINE.json north_star); 1 = flat searches run
- *                their UCB1 iterations after the root expansion inside one
- *                cooperative GPU kernel (same selections, same counts,
- *                ~2x fewer microseconds per iteration)
+ *                (default; BASELINE.json north_star); 1 = the whole search
+ *                runs in one cooperative GPU kernel per decision -- flat:
+ *                the UCB1 iterations after the root expansion (DESIGN.md
+ *                §R8); depth-capped: the tree lives in device memory (§R9).
+ *                Same selections, same counts; lower single-search latency,
+ *                but a search holds the GPU, so concurrent searches serialise
  * Returns DVC_E_CONFIG for an unknown name or a bad value. */
 int dvc_set_option(const char *name, int64_t value);
 int dvc_get_option(const char *name, int64_t *value);

@@ -14,25 +14,28 @@ from . import rollout as oracle_rollout, legal as oracle_legal
 LN2 = 0.6931471805599453        # the double nearest ln 2
 
 
+ATANH_C = [1.0 / (2 * k + 1) for k in range(14)]   # 1/(2k+1), each correctly rounded
+
+
 def ln_series(N):
     """ln N for an integer N >= 1 by a fixed IEEE-double recipe (DESIGN.md §R8,
     reading #28) that the C++ host tree and the CUDA search kernels evaluate
     operation for operation, so all three choose the same UCB1 child:
     N = m 2^e with m in [sqrt(1/2), sqrt(2)), ln N = 2 atanh(z) + e ln2 with
-    z = (m - 1)/(m + 1) (|z| < 0.172) and atanh(z) = sum_{k<14} z^(2k+1)/(2k+1),
-    summed in increasing k.  Accurate to ~1.5 ulp (tests/test_oracle_search.py)."""
+    z = (m - 1)/(m + 1) (|z| < 0.172) and atanh(z) = z * p(z^2), p the
+    14-term series sum_k z^(2k) / (2k+1) in Horner form (a multiply, then an
+    add, per term; no fused ops).  Accurate to ~1.5 ulp
+    (tests/test_oracle_search.py)."""
     m, e = math.frexp(float(N))
     if m < 0.7071067811865476:
         m *= 2.0
         e -= 1
     z = (m - 1.0) / (m + 1.0)
     z2 = z * z
-    s = 0.0
-    t = z
-    for k in range(14):
-        s += t / (2 * k + 1)
-        t *= z2
-    return 2.0 * s + e * LN2
+    p = ATANH_C[13]
+    for k in range(12, -1, -1):
+        p = p * z2 + ATANH_C[k]
+    return 2.0 * (z * p) + e * LN2
 
 
 def ucb1(wins, visits, parent_visits, c):

@@ -6,6 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <mutex>
@@ -25,6 +28,9 @@ cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaSt
 cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int mode, int block, size_t smem,
                              int *blocks_per_sm);
 cudaError_t search_occupancy(int P, bool jok, bool cons, bool inf, int block, size_t smem, int *blocks_per_sm);
+cudaError_t deep_occupancy(int P, bool jok, bool cons, int block, size_t smem, int *blocks_per_sm);
+cudaError_t launch_deep_search(const KParams &kp, const DeepArgs &da, int P, bool jok, bool cons, int grid,
+                               int block, size_t smem, cudaStream_t stream);
 cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, bool jok, bool cons, bool inf,
                                int grid, int block, size_t smem, cudaStream_t stream);
 
@@ -438,11 +444,127 @@ int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, c
   return DVC_OK;
 }
 
+// Device-resident depth-capped tree search: one cooperative
+// deep_search_kernel runs all `expansions` iterations; the host uploads the
+// candidate lists and reads back the root children's (visits, wins).
+int deep_search_gpu_impl(const dvc_state *s, const dvc_search_params *p, const uint32_t *root_codes, int32_t A_r,
+                         const uint32_t *deep_codes, int32_t A_d, uint64_t *visits, uint64_t *wins) {
+  const State *st = as_state(s);
+  if (!st) return set_err(DVC_E_CONFIG, "bad state");
+  const int P = st->P;
+  std::vector<uint32_t> lists((size_t)2 * (A_r + A_d));
+  const char *err = nullptr;
+  int rc = decode_actions(*st, root_codes, A_r, lists.data() + A_r, &err);
+  if (rc == DVC_OK && A_d > 0) rc = decode_deep(*st, deep_codes, A_d, lists.data() + 2 * A_r + A_d, &err);
+  if (rc) return set_err(rc, err ? err : "illegal action");
+  std::memcpy(lists.data(), root_codes, sizeof(uint32_t) * A_r);
+  std::memcpy(lists.data() + 2 * A_r, deep_codes, sizeof(uint32_t) * A_d);
+  const uint32_t max_batch = (uint32_t)(A_r > A_d ? A_r : A_d);
+  const uint64_t max_nodes = 1 + (uint64_t)p->expansions * max_batch;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t off_nn = al(max_nodes * sizeof(DNode)), off_b = off_nn + 256, off_l = off_b + al(sizeof(DBatch)),
+               off_w = off_l + al(lists.size() * 4), off_v = off_w + al(max_batch * 8),
+               off_o = off_v + al(max_batch * 8), off_st = off_o + al((size_t)A_r * 16), bytes = off_st + 256;
+  DeviceScratch *d = nullptr;
+  HostLane *L = nullptr;
+  std::vector<unsigned long long> out((size_t)2 * A_r);
+  int32_t status = 0;
+  std::lock_guard<std::mutex> lock(g_mu);
+  rc = get_scratch(p->device, &d);
+  if (rc) return rc;
+  rc = get_lane(d, 1, &L);
+  if (rc) return rc;
+  if (L->search_cap < bytes) {
+    if (L->d_search) cudaFree(L->d_search);
+    L->d_search = nullptr;
+    L->search_cap = 0;
+    cudaError_t e = cudaMalloc(&L->d_search, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(search)");
+    L->search_cap = bytes;
+  }
+  unsigned char *base = L->d_search;
+  cudaError_t e = cudaMemcpyAsync(base + off_l, lists.data(), lists.size() * 4, cudaMemcpyHostToDevice, L->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "search setup");
+  PlanEntry *plan = nullptr;
+  rc = get_plan(d, *st, L->stream, &plan);
+  if (rc) return rc;
+  KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  fill_kparams(kp, st, p->seed, 0u, 0u, plan, d);
+  DeepArgs da;
+  da.nodes = reinterpret_cast<DNode *>(base);
+  da.n_nodes = reinterpret_cast<uint32_t *>(base + off_nn);
+  da.batch = reinterpret_cast<DBatch *>(base + off_b);
+  const uint32_t *dl = reinterpret_cast<const uint32_t *>(base + off_l);
+  da.root_codes = dl;
+  da.root_meta = dl + A_r;
+  da.deep_codes = dl + 2 * A_r;
+  da.deep_meta = dl + 2 * A_r + A_d;
+  da.wins = reinterpret_cast<unsigned long long *>(base + off_w);
+  da.voids = reinterpret_cast<unsigned long long *>(base + off_v);
+  da.out = reinterpret_cast<unsigned long long *>(base + off_o);
+  da.status = reinterpret_cast<int32_t *>(base + off_st);
+  da.bar = reinterpret_cast<unsigned int *>(base + off_st + 64);
+  da.prof = std::getenv("DVC_DEEP_PROF") ? reinterpret_cast<unsigned long long *>(base + off_st + 128) : nullptr;
+  e = cudaMemsetAsync(base + off_st, 0, 256, L->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "search setup");
+  da.c = p->c;
+  da.n = (uint32_t)p->sims_per_child;
+  da.expansions = (uint32_t)p->expansions;
+  da.max_depth = (uint32_t)p->max_depth;
+  da.A_r = (uint32_t)A_r;
+  da.A_d = (uint32_t)A_d;
+  da.max_batch = max_batch;
+  da.max_nodes = (uint32_t)max_nodes;
+  const int block = 128;
+  const size_t smem = (size_t)max_batch * 8;
+  const uint64_t okey = (4ull << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
+                        ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)block << 32) | (uint64_t)smem;
+  int per_sm = 0;
+  auto it = d->occupancy.find(okey);
+  if (it != d->occupancy.end()) {
+    per_sm = it->second;
+  } else {
+    e = deep_occupancy(P, st->jokers != 0, st->consecutive != 0, block, smem, &per_sm);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    d->occupancy[okey] = per_sm;
+  }
+  if (per_sm < 1) return set_err(DVC_E_CONFIG, "deep search kernel cannot launch");
+  uint64_t grid = ((uint64_t)max_batch * da.n + block - 1) / block;
+  if (grid > (uint64_t)per_sm * d->num_sms) grid = (uint64_t)per_sm * d->num_sms;
+  e = launch_deep_search(kp, da, P, st->jokers != 0, st->consecutive != 0, (int)grid, block, smem, L->stream);
+  g_launches++;
+  if (e != cudaSuccess) return cuda_fail(e, "deep_search_kernel launch");
+  e = cudaMemcpyAsync(out.data(), da.out, out.size() * 8, cudaMemcpyDeviceToHost, L->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&status, da.status, 4, cudaMemcpyDeviceToHost, L->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "deep search");
+  if (da.prof) {
+    unsigned long long pr[5];
+    if (cudaMemcpy(pr, da.prof, sizeof(pr), cudaMemcpyDeviceToHost) == cudaSuccess && pr[4])
+      std::fprintf(stderr, "deep search per iteration (us): control %.1f barrier %.1f playouts %.1f barrier %.1f (%llu it, grid %d)\n",
+                   pr[0] / 1e3 / pr[4], pr[1] / 1e3 / pr[4], pr[2] / 1e3 / pr[4], pr[3] / 1e3 / pr[4], pr[4], (int)grid);
+  }
+  if (status == DVC_E_CONFIG) return set_err(status, "a node's sim index range would pass 2^32");
+  if (status == DVC_E_CAPACITY) return set_err(status, "deep search tree capacity");
+  if (status) return set_err(DVC_E_CUDA, "deep search kernel watchdog " + std::to_string(status));
+  for (int32_t a = 0; a < A_r; ++a) {
+    visits[a] = out[a];
+    wins[a] = out[(size_t)A_r + a];
+  }
+  return DVC_OK;
+}
+
 }  // namespace
 
 int set_error(int code, const char *msg) { return set_err(code, msg ? msg : ""); }
 
 bool search_on_device() { return g_search_device.load() != 0; }
+
+int deep_search_gpu(const dvc_state *s, const dvc_search_params *p, const uint32_t *root_codes, int32_t A_r,
+                    const uint32_t *deep_codes, int32_t A_d, uint64_t *visits, uint64_t *wins) {
+  return deep_search_gpu_impl(s, p, root_codes, A_r, deep_codes, A_d, visits, wins);
+}
 
 int flat_search_gpu(const dvc_state *s, const uint32_t *codes, int32_t A, const uint32_t *first, int32_t k,
                     const int32_t *batch_pos, const double *lnN, int32_t iters, const dvc_search_params *p,

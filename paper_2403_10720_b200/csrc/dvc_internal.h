@@ -82,6 +82,8 @@ int set_error(int code, const char *msg);
 double ln_series(uint64_t N);
 // Device flat search (api.cu): option "search_device", and the call itself.
 bool search_on_device();
+int deep_search_gpu(const dvc_state *s, const dvc_search_params *p, const uint32_t *root_codes, int32_t A_r,
+                    const uint32_t *deep_codes, int32_t A_d, uint64_t *visits, uint64_t *wins);
 int flat_search_gpu(const dvc_state *s, const uint32_t *codes, int32_t A, const uint32_t *first, int32_t k,
                     const int32_t *batch_pos, const double *lnN, int32_t iters, const dvc_search_params *p,
                     uint64_t *visits, uint64_t *wins);

@@ -94,7 +94,7 @@ __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_
 template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint4 B, uint32_t k,
                                                const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
-                                               const KParams &kp) {
+                                               const KParams &kp, uint32_t plen) {
   constexpr bool PATH = MODE == kModePath;
   turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
 #ifdef DVC_DEBUG
@@ -106,10 +106,10 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
   uint32_t t;
   bool correct;
   bool stop;
-  if (PATH && S.fi <= kp.path_len && S.g == kp.g0) {
+  if (PATH && S.fi <= plen && S.g == kp.g0) {
     // deep-tree batch: the viewer's next forced action F[fi] (the batch
     // action itself at fi == path_len) replaces the random decision
-    const uint32_t m = S.fi < kp.path_len ? path_of[S.fi] : meta_of_a[a];
+    const uint32_t m = S.fi < plen ? path_of[S.fi] : meta_of_a[a];
     bool illegal;
     stop = forced_decide<P, JOK, CONS>(S, m, kp, &t, &correct, &illegal);
     S.fi += 1;
@@ -141,7 +141,8 @@ template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
                                                  const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                  const KParams &kp) {
-  return step_block<P, JOK, CONS, MODE>(S, st, philox_rk(k, s, code, kp.node, kp), k, meta_of_a, path_of, a, kp);
+  return step_block<P, JOK, CONS, MODE>(S, st, philox_rk(k, s, code, kp.node, kp), k, meta_of_a, path_of, a, kp,
+                                        kp.path_len);
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
       uint4 B = philox_rk(0u, s, code, kp.node, kp);
       for (uint32_t k = 0; st != FINISH; ++k) {
         const uint4 Bn = philox_rk(k + 1u, s, code, kp.node, kp);
-        st = step_block<P, JOK, CONS, MODE>(S, st, B, k, nullptr, nullptr, 0, kp);
+        st = step_block<P, JOK, CONS, MODE>(S, st, B, k, nullptr, nullptr, 0, kp, 0u);
         B = Bn;
       }
       cnt += winner_seat(S) == kp.g0 ? 1u : 0u;
@@ -457,6 +458,323 @@ cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, b
   const void *f = select_search(P, jok, cons, inf);
   if (!f) return cudaErrorInvalidValue;
   void *args[] = {(void *)&kp, (void *)&sa};
+  return cudaLaunchCooperativeKernel(f, grid, block, args, smem, stream);
+}
+
+// ---- device-resident depth-capped tree search ----------------------------
+// dvc_mcts_search(flat = 0) with search_device = 1: the tree
+// lives in global memory and ONE cooperative kernel runs every iteration.
+// Block 0's warp 0 is the controller -- backpropagation of the last batch,
+// UCB1 descent (lanes score children, warp argmax; ln by ln_series_dev),
+// expansion, the next batch descriptor -- and the whole grid plays the batch
+// (F = path + [child], Philox keyed by the child's code and the batch node
+// word, exactly as dvc_rollout_path_ex) between two grid barriers.
+__device__ __forceinline__ double ln_series_dev(unsigned long long N) {
+  int e = 0;
+  double m = frexp((double)N, &e);
+  if (m < 0.7071067811865476) {
+    m = __dmul_rn(m, 2.0);
+    e -= 1;
+  }
+  const double z = __ddiv_rn(__dsub_rn(m, 1.0), __dadd_rn(m, 1.0));
+  const double z2 = __dmul_rn(z, z);
+  // Horner over the correctly rounded constants 1/(2k+1) (folded at compile time)
+  double p = 1.0 / 27.0;
+#pragma unroll
+  for (int k = 12; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, z2), 1.0 / (double)(2 * k + 1));
+  return __dadd_rn(__dmul_rn(2.0, __dmul_rn(z, p)), __dmul_rn((double)e, 0.6931471805599453));
+}
+
+__device__ __forceinline__ double ucb1_dev(unsigned long long w, unsigned long long v, double lnN, double c) {
+  return __dadd_rn(__ddiv_rn((double)w, (double)v), __dmul_rn(c, __dsqrt_rn(__ddiv_rn(lnN, (double)v))));
+}
+
+// Controller step, run by ALL threads of block 0 (block-uniform control flow,
+// __syncthreads between phases): backprop (thread 0), UCB1 descent (warp 0),
+// expansion / batch descriptor (thread 0), new children + zeroed counters (all).
+__device__ void control_step(const DeepArgs &da, uint32_t it) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  DNode *T = da.nodes;
+  DBatch *B = da.batch;
+  const uint32_t n = da.n;
+  __shared__ int32_t s_x;
+  __shared__ uint32_t s_stop;
+  __shared__ unsigned long long s_dv, s_dw;
+  // ---- backpropagation of the batch that just ran: the evaluated nodes in
+  // parallel, their sums to the ancestors by thread 0
+  if (it > 0) {
+    if (tid == 0) { s_dv = 0; s_dw = 0; }
+    __syncthreads();
+    const uint32_t nb = B->nb;
+    const int32_t e0 = B->eval0;
+    unsigned long long dv = 0, dw = 0;
+    for (uint32_t i = tid; i < nb; i += blockDim.x) {
+      DNode &e = T[e0 + (int32_t)i];
+      const unsigned long long vo = __ldcg(da.voids + i), wi = __ldcg(da.wins + i);
+      e.tried += n;
+      e.visits += n - vo;
+      e.wins += wi;
+      dv += n - vo;
+      dw += wi;
+    }
+    if (dv) atomicAdd(&s_dv, dv);
+    if (dw) atomicAdd(&s_dw, dw);
+    __syncthreads();
+    if (tid == 0)
+      for (int32_t y = T[e0].parent; y >= 0; y = T[y].parent) {
+        T[y].visits += s_dv;
+        T[y].wins += s_dw;
+      }
+  }
+  if (tid == 0) s_stop = it >= da.expansions ? 1u : 0u;
+  __syncthreads();
+  if (s_stop) {
+    if (tid == 0) B->stop = 1u;
+    __threadfence();
+    return;                                          // block-uniform
+  }
+  // ---- selection (warp 0): UCB1 descent, tried-but-never-non-void children skipped
+  if (tid < 32) {
+    int32_t x = 0;
+    for (int guard = 0; T[x].expanded && guard <= kMaxPath + 1; ++guard) {
+      const double lnN = ln_series_dev(T[x].visits);
+      double bv = 0.0;
+      uint32_t bi = 0xFFFFFFFFu, bcode = 0;
+      for (int32_t i = (int32_t)lane; i < T[x].nch; i += 32) {
+        const DNode &ch = T[T[x].first + i];
+        if (ch.tried > 0 && ch.visits == 0) continue;
+        const double v = ch.tried == 0 ? (double)INFINITY : ucb1_dev(ch.wins, ch.visits, lnN, da.c);
+        if (ucb_better(v, ch.code, (uint32_t)i, bv, bcode, bi)) { bv = v; bi = (uint32_t)i; bcode = ch.code; }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, off);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, off);
+        const uint32_t oc = __shfl_xor_sync(0xFFFFFFFFu, bcode, off);
+        if (ucb_better(ov, oc, oi, bv, bcode, bi)) { bv = ov; bi = oi; bcode = oc; }
+      }
+      if (bi == 0xFFFFFFFFu) break;
+      x = T[x].first + (int32_t)bi;
+    }
+    if (tid == 0) s_x = x;
+  }
+  __syncthreads();
+  const int32_t x = s_x;
+  // ---- expansion or re-simulation: the batch descriptor (thread 0)
+  if (tid == 0) {
+    DNode &X = T[x];
+    uint32_t pm[kMaxPath + 1];
+    uint32_t depth = 0;
+    for (int32_t y = x; y > 0 && depth <= kMaxPath; y = T[y].parent) pm[depth++] = T[y].meta;   // reversed
+    const bool expand = !X.expanded && X.depth < (int32_t)da.max_depth && (x == 0 || X.visits > 0);
+    uint32_t stop = 0u;
+    if (expand) {
+      const bool root = x == 0;
+      const uint32_t A = root ? da.A_r : da.A_d;
+      const int32_t first = (int32_t)da.n_nodes[0];
+      if ((uint32_t)first + A > da.max_nodes) {
+        stop = 1u;
+        *da.status = DVC_E_CAPACITY;
+      } else {
+        X.first = first;
+        X.nch = (int32_t)A;
+        X.expanded = 1u;
+        da.n_nodes[0] = (uint32_t)first + A;
+        B->nb = A;
+        B->eval0 = first;
+        B->node_word = (uint32_t)x;
+        B->plen = depth;
+        for (uint32_t i = 0; i < depth; ++i) B->path_meta[i] = pm[depth - 1 - i];
+        B->list = root ? 0u : 1u;
+      }
+    } else if (x == 0) {
+      stop = 1u;                                     // nothing left to do
+    } else {
+      B->nb = 1;
+      B->eval0 = x;
+      B->node_word = (uint32_t)X.parent;
+      B->plen = depth - 1;
+      for (uint32_t i = 0; i + 1 < depth; ++i) B->path_meta[i] = pm[depth - 1 - i];
+      B->list = 2u;
+      B->leaf_code = X.code;
+      B->leaf_meta = X.meta;
+    }
+    if (!stop) {
+      const unsigned long long s0 = expand ? 0ull : X.tried;     // new children start at sim 0
+      if (s0 + n > (1ull << 32)) {
+        stop = 1u;
+        *da.status = DVC_E_CONFIG;
+      }
+      B->s0 = (uint32_t)s0;
+    }
+    B->stop = stop;
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) {
+    __threadfence();
+    return;                                          // block-uniform
+  }
+  // ---- new children (all threads) and zeroed per-batch counters
+  const uint32_t nb = B->nb;
+  if (B->list != 2u) {
+    const bool root = B->list == 0u;
+    const uint32_t *codes = root ? da.root_codes : da.deep_codes;
+    const uint32_t *metas = root ? da.root_meta : da.deep_meta;
+    const int32_t first = B->eval0;
+    const int32_t cdepth = T[x].depth + 1;
+    for (uint32_t i = tid; i < nb; i += blockDim.x) {
+      DNode &c = T[first + (int32_t)i];
+      c.visits = 0; c.wins = 0; c.tried = 0;
+      c.code = codes[i]; c.meta = metas[i];
+      c.parent = x; c.depth = cdepth; c.first = -1; c.nch = 0; c.expanded = 0u;
+    }
+  }
+  for (uint32_t i = tid; i < nb; i += blockDim.x) { da.wins[i] = 0; da.voids[i] = 0; }
+  __threadfence();
+  __syncthreads();
+}
+
+constexpr int32_t kWatchdogBarrier = 101, kWatchdogPlayout = 102;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Grid barrier with a watchdog (cooperative launch => all blocks resident):
+// returns false (and records `code` in *status) if the other blocks do not
+// arrive within about a minute, so a logic error ends the kernel with an
+// error instead of hanging the device.
+__device__ bool grid_barrier(unsigned int *bar, int32_t *status, int32_t code) {
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    volatile unsigned int *gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1u) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const long long t0 = clock64();
+      while (*gen == g) {
+        if (clock64() - t0 > 120000000000ll) { atomicCAS(status, 0, code); s_ok = 0; break; }   // ~1 min
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+template <int P, bool JOK, bool CONS>
+__global__ void __launch_bounds__(128) deep_search_kernel(const __grid_constant__ KParams kp,
+                                                          const __grid_constant__ DeepArgs da) {
+  extern __shared__ uint32_t shd[];
+  uint32_t *swin = shd, *svoid = shd + da.max_batch;
+  __shared__ uint32_t s_path[kMaxPath];
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gsize = gridDim.x * blockDim.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    DNode &r = da.nodes[0];
+    r.visits = 0; r.wins = 0; r.tried = 0; r.code = 0; r.meta = 0;
+    r.parent = -1; r.depth = 0; r.first = -1; r.nch = 0; r.expanded = 0u;
+    da.n_nodes[0] = 1u;
+    *da.status = 0;
+  }
+  unsigned long long t_mark = 0;
+  for (uint32_t it = 0;; ++it) {
+    if (da.prof && blockIdx.x == 0 && threadIdx.x == 0) t_mark = globaltimer_ns();
+    if (blockIdx.x == 0) control_step(da, it);
+    if (da.prof && blockIdx.x == 0 && threadIdx.x == 0) { const auto t = globaltimer_ns(); da.prof[0] += t - t_mark; t_mark = t; }
+    if (!grid_barrier(da.bar, da.status, kWatchdogBarrier)) return;
+    if (da.prof && blockIdx.x == 0 && threadIdx.x == 0) { const auto t = globaltimer_ns(); da.prof[1] += t - t_mark; t_mark = t; }
+    const DBatch *B = da.batch;
+    if (__ldcg(&B->stop)) break;
+    // ---- the batch: nb actions x n sims, F = path + [action]
+    const uint32_t nb = __ldcg(&B->nb), plen = __ldcg(&B->plen), list = __ldcg(&B->list);
+    const uint32_t node = __ldcg(&B->node_word), s0 = __ldcg(&B->s0);
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) { swin[i] = 0; svoid[i] = 0; }
+    if (threadIdx.x < kMaxPath) s_path[threadIdx.x] = __ldcg(&B->path_meta[threadIdx.x]);
+    __syncthreads();
+    const uint32_t *codes = list == 0u ? da.root_codes : da.deep_codes;
+    const uint32_t *metas = list == 0u ? da.root_meta : da.deep_meta;
+    const uint32_t lcode = __ldcg(&B->leaf_code), lmeta = __ldcg(&B->leaf_meta);
+    const uint32_t total = nb * da.n;
+    for (uint32_t w = gtid; w < total; w += gsize) {
+      const uint32_t a = w / da.n, s = s0 + (w - a * da.n);
+      const uint32_t code = list == 2u ? lcode : codes[a], meta = list == 2u ? lmeta : metas[a];
+      Sim<P> S;
+      const uint4 D = philox_rk(0xFFFFFFFFu, s, code, node, kp);
+      determinize<P>(S, D, kp);
+      uint32_t t;
+      bool correct;
+      const bool stop = root_action<P, JOK>(S, plen ? s_path[0] : meta, kp, &t, &correct);
+      S.fi = 1;
+      uint32_t st = stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
+      const uint32_t meta_a[1] = {meta};
+      for (uint32_t k = 0; st != FINISH && st != VOID; ++k) {
+        st = step_block<P, JOK, CONS, kModePath>(S, st, philox_rk(k, s, code, node, kp), k, meta_a, s_path, 0u,
+                                                  kp, plen);
+        if (k > 4096u) { atomicCAS(da.status, 0, kWatchdogPlayout); st = VOID; }   // never expected
+      }
+      if (st == VOID || S.fi <= plen) atomicAdd(&svoid[a], 1u);
+      else if (winner_seat(S) == kp.g0) atomicAdd(&swin[a], 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+      if (swin[i]) atomicAdd(da.wins + i, (unsigned long long)swin[i]);
+      if (svoid[i]) atomicAdd(da.voids + i, (unsigned long long)svoid[i]);
+    }
+    if (da.prof && blockIdx.x == 0 && threadIdx.x == 0) { const auto t = globaltimer_ns(); da.prof[2] += t - t_mark; t_mark = t; }
+    if (!grid_barrier(da.bar, da.status, kWatchdogBarrier)) return;
+    if (da.prof && blockIdx.x == 0 && threadIdx.x == 0) { const auto t = globaltimer_ns(); da.prof[3] += t - t_mark; da.prof[4] += 1; }
+  }
+  if (blockIdx.x == 0) {
+    // root children (created in LEGAL order by the first expansion)
+    const DNode &r = da.nodes[0];
+    for (uint32_t i = threadIdx.x; i < da.A_r; i += blockDim.x) {
+      const bool has = r.expanded && (int32_t)i < r.nch;
+      da.out[i] = has ? da.nodes[r.first + (int32_t)i].visits : 0ull;
+      da.out[da.A_r + i] = has ? da.nodes[r.first + (int32_t)i].wins : 0ull;
+    }
+  }
+}
+
+template <int P, bool JOK, bool CONS>
+const void *deep_fn() { return (const void *)deep_search_kernel<P, JOK, CONS>; }
+
+const void *select_deep(int P, bool jok, bool cons) {
+#define DVC_DCASE(PP)                                                                   \
+  if (P == PP) {                                                                        \
+    if (jok) return cons ? deep_fn<PP, true, true>() : deep_fn<PP, true, false>();     \
+    return cons ? deep_fn<PP, false, true>() : deep_fn<PP, false, false>();            \
+  }
+  DVC_DCASE(2)
+  DVC_DCASE(3)
+  DVC_DCASE(4)
+#undef DVC_DCASE
+  return nullptr;
+}
+
+cudaError_t deep_occupancy(int P, bool jok, bool cons, int block, size_t smem, int *blocks_per_sm) {
+  const void *f = select_deep(P, jok, cons);
+  if (!f) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+}
+
+cudaError_t launch_deep_search(const KParams &kp, const DeepArgs &da, int P, bool jok, bool cons, int grid,
+                               int block, size_t smem, cudaStream_t stream) {
+  const void *f = select_deep(P, jok, cons);
+  if (!f) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  void *args[] = {(void *)&kp, (void *)&da};
   return cudaLaunchCooperativeKernel(f, grid, block, args, smem, stream);
 }
 

@@ -49,12 +49,9 @@ double ln_series(uint64_t N) {
   }
   const double z = (m - 1.0) / (m + 1.0);
   const double z2 = z * z;
-  double s = 0.0, t = z;
-  for (int k = 0; k < 14; ++k) {
-    s += t / (double)(2 * k + 1);
-    t *= z2;
-  }
-  return 2.0 * s + (double)e * 0.6931471805599453;
+  double p = 1.0 / 27.0;
+  for (int k = 12; k >= 0; --k) p = p * z2 + 1.0 / (double)(2 * k + 1);
+  return 2.0 * (z * p) + (double)e * 0.6931471805599453;
 }
 }  // namespace dvc
 
@@ -74,6 +71,13 @@ int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p,
   std::vector<uint32_t> deep_codes;
   for (uint32_t c : root_codes) if (c != DVC_STOP) deep_codes.push_back(c);
   if (st->consecutive) deep_codes.push_back(DVC_STOP);
+  if (search_on_device()) {
+    // the same tree, iterations and batches in one cooperative GPU kernel
+    rv.assign(root_codes.size(), 0);
+    rw.assign(root_codes.size(), 0);
+    return deep_search_gpu(s, p, root_codes.data(), (int32_t)root_codes.size(), deep_codes.data(),
+                           (int32_t)deep_codes.size(), rv.data(), rw.data());
+  }
   std::vector<Node> T;
   T.push_back(Node{0u, 0, -1});
   std::vector<uint64_t> hist, voids;

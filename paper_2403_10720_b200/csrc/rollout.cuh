@@ -69,6 +69,33 @@ struct SearchArgs {
   uint32_t iters;                        // iterations after the root expansion
 };
 
+// Device depth-capped tree search (kernels.cu deep_search_kernel).
+struct DNode {
+  unsigned long long visits, wins, tried;
+  uint32_t code, meta;      // the guess and its act_meta (root meta at depth 1, deep meta below)
+  int32_t parent, depth, first, nch;   // children are T[first, first + nch)
+  uint32_t expanded, _pad;
+};
+struct DBatch {
+  uint32_t stop, nb, node_word, s0, plen, list;   // list: 0 root codes, 1 deep codes, 2 the leaf alone
+  int32_t eval0;                                  // first evaluated node (children are contiguous)
+  uint32_t leaf_code, leaf_meta;
+  uint32_t path_meta[kMaxPath];
+};
+struct DeepArgs {
+  DNode *nodes;
+  uint32_t *n_nodes;                     // [1] nodes in use
+  DBatch *batch;
+  const uint32_t *root_codes, *root_meta, *deep_codes, *deep_meta;
+  unsigned long long *wins, *voids;      // [max_batch] this batch's viewer wins / void playouts
+  unsigned long long *out;               // [2 * A_r] root children visits, then wins (LEGAL order)
+  int32_t *status;                       // 0, or a DVC_E_* code that stopped the search
+  unsigned int *bar;                     // [2] grid barrier (arrivals, generation), zeroed
+  unsigned long long *prof;              // DVC_DEEP_PROF: [control, barrier, playouts, barrier, iters] ns, or null
+  double c;
+  uint32_t n, expansions, max_depth, A_r, A_d, max_batch, max_nodes;
+};
+
 // ----------------------------------------------------------------- RNG (§R3)
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                                uint32_t k0, uint32_t k1) {

@@ -104,26 +104,55 @@ def test_path_batches_equal_oracle(dvc, oracle_lib, path, kernel):
 
 
 @pytest.mark.parametrize("path", CASES[:6], ids=[os.path.basename(p) for p in CASES[:6]])
-def test_deep_search_equals_oracle(dvc, oracle_lib, path):
+@pytest.mark.parametrize("sdev", [0, 1], ids=["host_tree", "device_tree"])
+def test_deep_search_equals_oracle(dvc, oracle_lib, path, sdev):
     from oracle.search import deep_search
     d = json.load(open(os.path.join(ROOT, path)))
     P = d["rules"]["players"]
     exp_n, n = (5, 48) if P == 4 else (8, 128)
     best_o, stats_o = deep_search(d, exp_n, n, 33, max_depth=3)
     st = dvc.encode(d)
-    best_g, stats_g = dvc.mcts_search(st, exp_n, n, 33, max_depth=3, flat=0)
+    with dvc.options(search_device=sdev):
+        best_g, stats_g = dvc.mcts_search(st, exp_n, n, 33, max_depth=3, flat=0)
     assert [tuple(map(int, t)) for t in stats_g] == stats_o
     assert best_g == best_o
 
 
-@pytest.mark.parametrize("flat,seed", [(1, 1), (1, 2), (0, 3)])
-def test_selfplay_equals_oracle(dvc, oracle_lib, flat, seed):
+DEEP_DEV = [("fixtures/c3_d1.json", 40, 300, 4), ("fixtures/c2_d2.json", 60, 200, 3),
+            ("tests/golden/T2c1.json", 50, 100, 4), ("fixtures/xstop_d1.json", 30, 150, 2),
+            ("fixtures/x3_d1.json", 20, 100, 4), ("fixtures/c4_d5.json", 12, 60, 3),
+            ("fixtures/xsmall_d3.json", 80, 64, 8), ("fixtures/c1_d1.json", 25, 333, 1)]
+
+
+@pytest.mark.parametrize("path,exp_n,n,depth", DEEP_DEV, ids=[os.path.basename(c[0]) for c in DEEP_DEV])
+def test_device_tree_equals_host_tree_and_oracle(dvc, oracle_lib, path, exp_n, n, depth):
+    """The cooperative deep_search_kernel (search_device=1: tree in device
+    memory, UCB1 descent / expansion / backprop by one warp, batches over the
+    grid) reproduces the host tree (search_device=0) and the oracle's
+    deep_search exactly, over many iterations, depths 1..8 and void-heavy
+    trees."""
+    from oracle.search import deep_search
+    d = json.load(open(os.path.join(ROOT, path)))
+    st = dvc.encode(d)
+    with dvc.options(search_device=1):
+        best_d, stats_d = dvc.mcts_search(st, exp_n, n, 61, max_depth=depth, flat=0)
+    with dvc.options(search_device=0):
+        best_h, stats_h = dvc.mcts_search(st, exp_n, n, 61, max_depth=depth, flat=0)
+    stats_d = [tuple(map(int, t)) for t in stats_d]
+    assert stats_d == [tuple(map(int, t)) for t in stats_h] and best_d == best_h
+    best_o, stats_o = deep_search(d, exp_n, n, 61, max_depth=depth)
+    assert stats_d == stats_o and best_d == best_o
+
+
+@pytest.mark.parametrize("flat,seed,sdev", [(1, 1, 0), (1, 2, 1), (0, 3, 0), (0, 4, 1)])
+def test_selfplay_equals_oracle(dvc, oracle_lib, flat, seed, sdev):
     """C3 shape (2 players, 26 tiles with jokers): a full self-play game with
     the GPU searches reproduces the oracle's game move for move."""
     from paper_2403_10720_b200.selfplay import play_game
     from oracle.selfplay import play_game as oracle_game
     kw = dict(expansions=6, sims_per_child=64, flat=flat, max_depth=2)
-    g = play_game(seed, **kw)
+    with dvc.options(search_device=sdev):
+        g = play_game(seed, **kw)
     o = oracle_game(seed, **kw)
     assert g == o
     assert g["decisions"] >= 2

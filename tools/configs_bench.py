@@ -84,7 +84,8 @@ def main():
         from paper_2403_10720_b200.selfplay import play_game
         for flat, sdev, label in ((1, 1, "flat UCT (root-parallel, PAPER:180), device-resident UCB loop"),
                                   (1, 0, "flat UCT (root-parallel, PAPER:180), host UCB loop"),
-                                  (0, 0, "depth-capped tree, max_depth 4")):
+                                  (0, 0, "depth-capped tree, max_depth 4, host tree"),
+                                  (0, 1, "depth-capped tree, max_depth 4, device-resident tree")):
             dvc.set_option("search_device", sdev)
             rows = []
             dvc.mcts_search(dvc.encode(load("c3_d*.json")[0]), 4, 1024, 5, flat=flat)
