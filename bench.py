@@ -224,6 +224,60 @@ def run_reference(args):
     return 0
 
 
+def run_reference_sweep(args):
+    """The reference arm's sweeps for the paper's CPU experiments (driven by
+    tools/paper_experiments.py, which never touches oracle/ itself); one JSON
+    row per run, SPEC:370 columns:
+      exp1: `--ref-sizes` total simulations over the C2 workload's actions
+            (the first n mod A actions get one more), all host cores;
+      exp2: simulations/s vs worker processes 1 .. 2 x cores."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    d = load_workload()
+    codes = oracle.legal(d)
+    A = len(codes)
+    cores = os.cpu_count() or 1
+
+    def emit(run, workers, total, t_s):
+        print(json.dumps({"run": run, "workers": workers, "total_simulations": total, "elapsed_ns": int(t_s * 1e9),
+                          "sims_per_sec": total / t_s, "device": "cpu", "kernel": "oracle"}), flush=True)
+
+    if args.ref_sweep == "exp1":
+        with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as ex:
+            list(ex.map(_oracle_job, [(d, codes, 1, 0, 1)] * cores))          # warm the workers
+            for n in [int(x) for x in args.ref_sizes.split(",")]:
+                per, extra = divmod(n, A)
+                ts = []
+                for r in range(args.steps):
+                    jobs = [(d, codes, 1 + r, (per * w) // cores, (per * (w + 1)) // cores) for w in range(cores)]
+                    jobs = [j for j in jobs if j[4] > j[3]]
+                    if extra:
+                        jobs.append((d, codes[:extra], 1 + r, per, per + 1))
+                    t0 = time.perf_counter()
+                    list(ex.map(_oracle_job, jobs))
+                    ts.append(time.perf_counter() - t0)
+                    emit(r, cores, n, ts[-1])
+                emit(-1, cores, n, sum(ts) / len(ts))
+    else:
+        n_per_worker = 4000
+        for w in sorted({1, 2, 4, 8, 12, 16, 24, 32, cores, 2 * cores}):
+            if w > 2 * cores:
+                continue
+            with ProcessPoolExecutor(max_workers=w, mp_context=mp.get_context("spawn")) as ex:
+                list(ex.map(_oracle_job, [(d, codes[:1], 1, 0, 1)] * w))
+                ts = []
+                for r in range(args.steps):
+                    jobs = [(d, codes[:4], 1 + r, i * n_per_worker, (i + 1) * n_per_worker) for i in range(w)]
+                    t0 = time.perf_counter()
+                    list(ex.map(_oracle_job, jobs))
+                    ts.append(time.perf_counter() - t0)
+                    emit(r, w, w * n_per_worker * 4, ts[-1])
+                emit(-1, w, w * n_per_worker * 4, sum(ts) / len(ts))
+    return 0
+
+
 # ----------------------------------------------------------------- product arm
 def run_product(args):
     import torch
@@ -383,9 +437,12 @@ def main():
     ap.add_argument("--sims", type=int, default=SIMS_PER_ACTION)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sweep", choices=["exp1", "exp2"], default=None,
+                    help="reference arm: the paper's CPU experiment sweeps (tools/paper_experiments.py)")
+    ap.add_argument("--ref-sizes", default="1,10,100,1000,10000,100000,1000000")
     args = ap.parse_args()
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference_sweep(args) if args.ref_sweep else run_reference(args)
     return run_product(args)
 
 

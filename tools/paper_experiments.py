@@ -23,10 +23,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def _job(args):
-    import oracle
-    d, codes, seed, s0, s1 = args
-    return oracle.rollout(d, codes, seed, 0, s0, s1)
+def cpu_rows(exp, steps, sizes=None):
+    """The CPU (oracle) side runs in bench.py's reference arm (the only place
+    besides tests/ allowed to execute oracle/); returns its rows."""
+    import subprocess
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--ref-sweep", exp,
+           "--steps", str(steps)]
+    if sizes:
+        cmd += ["--ref-sizes", ",".join(map(str, sizes))]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True, cwd=ROOT).stdout
+    return [json.loads(l) for l in out.splitlines() if l.startswith("{")]
 
 
 def main():
@@ -36,12 +42,8 @@ def main():
     ap.add_argument("--cpu-max", type=int, default=1_000_000)
     ap.add_argument("--repeats", type=int, default=5)
     args = ap.parse_args()
-    from concurrent.futures import ProcessPoolExecutor
-    import multiprocessing as mp
     import torch
-    import oracle
     from paper_2403_10720_b200 import dvc
-    oracle.build()
     d = json.load(open(os.path.join(ROOT, "fixtures", "c2_d1.json")))
     st = dvc.encode(d)
     codes = st.legal_actions()
@@ -55,8 +57,6 @@ def main():
     sizes = [1, 10, 100, 1000, 10 ** 4, 10 ** 5, 10 ** 6, 10 ** 7]
     hist = torch.zeros((A, st.players), dtype=torch.int64, device="cuda")
     stream = torch.cuda.current_stream()
-    pool = ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn"))
-    list(pool.map(_job, [(d, codes, 1, 0, 1)] * cores))                  # warm the workers
     for n in sizes:
         # GPU: n simulations over the actions (the first n mod A actions get one more)
         per, extra = divmod(n, A)
@@ -79,50 +79,17 @@ def main():
             rows.append((i, 1, n, int(t), n / (t / 1e9), "B200", "refill"))
         rows.append((-1, 1, n, int(sum(ts) / len(ts)), n / (sum(ts) / len(ts) / 1e9), "B200", "refill"))
         print(json.dumps({"exp": 1, "device": "gpu", "sims": n, "mean_ms": sum(ts) / len(ts) / 1e6}), flush=True)
-        if n <= args.cpu_max:
-            ts = []
-            for r in range(args.repeats):
-                jobs = []
-                for w in range(cores):
-                    a0, a1 = (per * w) // cores, (per * (w + 1)) // cores
-                    if a1 > a0:
-                        jobs.append((d, codes, 1 + r, a0, a1))
-                if extra:
-                    jobs.append((d, codes[:extra], 1 + r, per, per + 1))
-                t0 = time.perf_counter()
-                list(pool.map(_job, jobs))
-                ts.append((time.perf_counter() - t0) * 1e9)
-            for i, t in enumerate(ts):
-                rows.append((i, cores, n, int(t), n / (t / 1e9), "cpu", "oracle"))
-            rows.append((-1, cores, n, int(sum(ts) / len(ts)), n / (sum(ts) / len(ts) / 1e9), "cpu", "oracle"))
-            print(json.dumps({"exp": 1, "device": "cpu", "workers": cores, "sims": n,
-                              "mean_ms": sum(ts) / len(ts) / 1e6}), flush=True)
-    pool.shutdown()
+    for r in cpu_rows("exp1", args.repeats, [n for n in sizes if n <= args.cpu_max]):
+        rows.append((r["run"], r["workers"], r["total_simulations"], r["elapsed_ns"], r["sims_per_sec"], "cpu",
+                     "oracle"))
     with open(os.path.join(args.out, "%s_exp1_time_vs_sims.csv" % args.tag), "w") as f:
         f.write(hdr)
         for r in rows:
             f.write("%d,%d,%d,%d,%.6e,%s,%s\n" % r)
 
-    # ---- EXP-2: CPU sims/s vs workers
-    rows = []
-    n_per_worker = 4000
-    for w in sorted({1, 2, 4, 8, 12, 16, 24, 32, cores, 2 * cores}):
-        if w > 2 * cores:
-            continue
-        with ProcessPoolExecutor(max_workers=w, mp_context=mp.get_context("spawn")) as ex:
-            list(ex.map(_job, [(d, codes[:1], 1, 0, 1)] * w))
-            ts = []
-            for r in range(3):
-                jobs = [(d, codes[:4], 1 + r, i * n_per_worker, (i + 1) * n_per_worker) for i in range(w)]
-                t0 = time.perf_counter()
-                list(ex.map(_job, jobs))
-                ts.append(time.perf_counter() - t0)
-            total = w * n_per_worker * 4
-            for i, t in enumerate(ts):
-                rows.append((i, w, total, int(t * 1e9), total / t, "cpu", "oracle"))
-            m = sum(ts) / len(ts)
-            rows.append((-1, w, total, int(m * 1e9), total / m, "cpu", "oracle"))
-            print(json.dumps({"exp": 2, "workers": w, "sims_per_s": total / m}), flush=True)
+    # ---- EXP-2: CPU sims/s vs workers (bench.py reference arm)
+    rows = [(r["run"], r["workers"], r["total_simulations"], r["elapsed_ns"], r["sims_per_sec"], "cpu", "oracle")
+            for r in cpu_rows("exp2", 3)]
     with open(os.path.join(args.out, "%s_exp2_cpu_workers.csv" % args.tag), "w") as f:
         f.write(hdr)
         for r in rows:
