@@ -49,9 +49,14 @@ int set_err(int code, const std::string &msg) {
 struct PlanEntry {
   uint64_t hash;
   uint8_t *d_plan = nullptr;
+  size_t plan_cap = 0;
   uint4 *d_table = nullptr;   // null if N > table_cap when built
+  size_t table_cap = 0;
   uint64_t N = 0;
   cudaEvent_t ready = nullptr;  // recorded after plan upload + table build
+  // the last launch reading this plan on each stream: an evicted plan's
+  // buffers are reused only once all of these have completed
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
   std::vector<uint8_t> host_img;
 };
 
@@ -77,6 +82,9 @@ struct DeviceScratch {
   uint32_t *d_debug = nullptr;           // DVC_DEBUG builds: invariant counters
   std::unordered_map<std::thread::id, HostLane> lanes;
   std::list<PlanEntry> plans;            // LRU, front = most recent
+  std::list<PlanEntry> zombies;          // evicted, possibly still read by in-flight launches
+  std::vector<std::pair<void *, size_t>> pool;   // reclaimed device buffers (best fit)
+  std::vector<cudaEvent_t> events;       // reclaimed events
   std::unordered_map<uint64_t, int> occupancy;   // resident blocks per SM per launch shape
 };
 
@@ -142,12 +150,107 @@ int get_lane(DeviceScratch *d, size_t n, HostLane **out) {
   return DVC_OK;
 }
 
-void free_plan(PlanEntry &p) {
-  if (p.ready) cudaEventSynchronize(p.ready);
+// ---- plan memory: pooled device buffers and events, reclaimed by completion
+// events instead of a device-wide synchronisation (concurrent host threads'
+// launches keep running while a plan is evicted).
+constexpr size_t kPoolMaxBytes = 512ull << 20;
+constexpr size_t kZombieMax = 8;
+
+void *pool_get(DeviceScratch *d, size_t bytes, size_t *cap, cudaError_t *err) {
+  size_t bi = d->pool.size();
+  for (size_t i = 0; i < d->pool.size(); ++i) {
+    const size_t c = d->pool[i].second;
+    if (c >= bytes && c <= 4 * bytes + 4096 && (bi == d->pool.size() || c < d->pool[bi].second)) bi = i;
+  }
+  if (bi < d->pool.size()) {
+    void *p = d->pool[bi].first;
+    *cap = d->pool[bi].second;
+    d->pool.erase(d->pool.begin() + (long)bi);
+    *err = cudaSuccess;
+    return p;
+  }
+  void *p = nullptr;
+  *err = cudaMalloc(&p, bytes);
+  *cap = bytes;
+  return *err == cudaSuccess ? p : nullptr;
+}
+
+void pool_put(DeviceScratch *d, void *p, size_t cap) {
+  if (!p) return;
+  d->pool.push_back({p, cap});
+  size_t total = 0;
+  for (auto &b : d->pool) total += b.second;
+  while (total > kPoolMaxBytes && !d->pool.empty()) {
+    size_t li = 0;
+    for (size_t i = 1; i < d->pool.size(); ++i) if (d->pool[i].second > d->pool[li].second) li = i;
+    total -= d->pool[li].second;
+    cudaFree(d->pool[li].first);
+    d->pool.erase(d->pool.begin() + (long)li);
+  }
+}
+
+cudaError_t event_get(DeviceScratch *d, cudaEvent_t *ev) {
+  if (!d->events.empty()) {
+    *ev = d->events.back();
+    d->events.pop_back();
+    return cudaSuccess;
+  }
+  return cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+}
+
+bool plan_idle(const PlanEntry &p) {
+  if (p.ready && cudaEventQuery(p.ready) == cudaErrorNotReady) return false;
+  for (auto &u : p.uses)
+    if (cudaEventQuery(u.second) == cudaErrorNotReady) return false;
+  return true;
+}
+
+void reclaim(DeviceScratch *d, PlanEntry &p) {
+  pool_put(d, p.d_plan, p.plan_cap);
+  pool_put(d, p.d_table, p.table_cap);
+  if (p.ready) d->events.push_back(p.ready);
+  for (auto &u : p.uses) d->events.push_back(u.second);
+  p.d_plan = nullptr; p.d_table = nullptr; p.ready = nullptr;
+  p.uses.clear();
+}
+
+// Reclaim evicted plans whose launches have finished; past kZombieMax, wait
+// for the oldest one's own events (not the whole device).
+void reap(DeviceScratch *d) {
+  for (auto it = d->zombies.begin(); it != d->zombies.end();) {
+    if (plan_idle(*it)) { reclaim(d, *it); it = d->zombies.erase(it); } else { ++it; }
+  }
+  while (d->zombies.size() > kZombieMax) {
+    PlanEntry &p = d->zombies.back();
+    if (p.ready) cudaEventSynchronize(p.ready);
+    for (auto &u : p.uses) cudaEventSynchronize(u.second);
+    reclaim(d, p);
+    d->zombies.pop_back();
+  }
+}
+
+// Record that a launch just enqueued on `stream` reads plan p (caller holds g_mu).
+int note_use(DeviceScratch *d, PlanEntry *p, cudaStream_t stream) {
+  for (auto &u : p->uses)
+    if (u.first == stream) {
+      cudaError_t e = cudaEventRecord(u.second, stream);
+      return e == cudaSuccess ? DVC_OK : cuda_fail(e, "cudaEventRecord(use)");
+    }
+  cudaEvent_t ev;
+  cudaError_t e = event_get(d, &ev);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(use)");
+  p->uses.push_back({stream, ev});
+  return DVC_OK;
+}
+
+void free_plan_now(PlanEntry &p) {                 // shutdown only (device already synchronised)
   if (p.d_plan) cudaFree(p.d_plan);
   if (p.d_table) cudaFree(p.d_table);
   if (p.ready) cudaEventDestroy(p.ready);
+  for (auto &u : p.uses) cudaEventDestroy(u.second);
   p.d_plan = nullptr; p.d_table = nullptr; p.ready = nullptr;
+  p.uses.clear();
 }
 
 // Plan (+ table) for this state on this device; built on `stream` on first use,
@@ -162,7 +265,11 @@ int get_plan(DeviceScratch *d, const State &st, cudaStream_t stream, PlanEntry *
       cudaError_t e = cudaStreamWaitEvent(stream, p.ready, 0);
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
       if (!g_plan_cache.load()) {
-        // recompute per call (no cross-call reuse): plan upload + table build
+        // recompute per call (no cross-call reuse): plan upload + table build,
+        // after every launch that still reads the old contents
+        for (auto &u : p.uses)
+          if (u.first != stream && (e = cudaStreamWaitEvent(stream, u.second, 0)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamWaitEvent(use)");
         e = cudaMemcpyAsync(p.d_plan, p.host_img.data(), p.host_img.size(), cudaMemcpyHostToDevice, stream);
         if (e == cudaSuccess && p.d_table) {
           e = launch_table(p.d_plan, p.N, p.d_table, stream);
@@ -175,31 +282,31 @@ int get_plan(DeviceScratch *d, const State &st, cudaStream_t stream, PlanEntry *
       return DVC_OK;
     }
   }
+  reap(d);
   PlanEntry p;
   p.hash = h;
   p.N = build_plan(st, &p.host_img);
   if (p.N != st.N) return set_err(DVC_E_INCONSISTENT, "determinization count changed (corrupt state?)");
-  cudaError_t e = cudaMalloc(&p.d_plan, p.host_img.size());
+  cudaError_t e;
+  p.d_plan = static_cast<uint8_t *>(pool_get(d, p.host_img.size(), &p.plan_cap, &e));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(plan)");
   e = cudaMemcpyAsync(p.d_plan, p.host_img.data(), p.host_img.size(), cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaMemcpyAsync(plan)"); }
+  if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "cudaMemcpyAsync(plan)"); }
   if (p.N <= cap) {
-    e = cudaMalloc(&p.d_table, p.N * sizeof(uint4));
-    if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaMalloc(table)"); }
+    p.d_table = static_cast<uint4 *>(pool_get(d, p.N * sizeof(uint4), &p.table_cap, &e));
+    if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "cudaMalloc(table)"); }
     e = launch_table(p.d_plan, p.N, p.d_table, stream);
     g_launches++;
-    if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "det_table_kernel"); }
+    if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "det_table_kernel"); }
   }
-  e = cudaEventCreateWithFlags(&p.ready, cudaEventDisableTiming);
+  e = event_get(d, &p.ready);
   if (e == cudaSuccess) e = cudaEventRecord(p.ready, stream);
-  if (e != cudaSuccess) { free_plan(p); return cuda_fail(e, "cudaEventRecord"); }
+  if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "cudaEventRecord"); }
   d->plans.push_front(std::move(p));
   while (d->plans.size() > kPlanCacheMax) {
-    // kernels on other host threads' streams may still read the evicted
-    // plan/table: drain the device before freeing (rare: > 16 live states)
-    cudaDeviceSynchronize();
-    free_plan(d->plans.back());
-    d->plans.pop_back();
+    // evicted plans may still be read by launches on other host threads'
+    // streams: they wait in `zombies` until their use events complete
+    d->zombies.splice(d->zombies.begin(), d->plans, std::prev(d->plans.end()));
   }
   *out = &d->plans.front();
   return DVC_OK;
@@ -343,7 +450,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     if (e != cudaSuccess) return cuda_fail(e, "rollout kernel launch");
     b = e_;
   }
-  return DVC_OK;
+  return note_use(d, plan, stream);
 }
 
 // Device-resident flat search: the root-expansion batch (the
@@ -432,6 +539,8 @@ int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, c
                                        block, smem, L->stream);
     g_launches++;
     if (e != cudaSuccess) return cuda_fail(e, "flat_search_kernel launch");
+    rc = note_use(d, plan, L->stream);
+    if (rc) return rc;
     e = cudaMemcpyAsync(out.data(), sa.out, out.size() * 8, cudaMemcpyDeviceToHost, L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "search readback");
   }
@@ -535,6 +644,8 @@ int deep_search_gpu_impl(const dvc_state *s, const dvc_search_params *p, const u
   e = launch_deep_search(kp, da, P, st->jokers != 0, st->consecutive != 0, (int)grid, block, smem, L->stream);
   g_launches++;
   if (e != cudaSuccess) return cuda_fail(e, "deep_search_kernel launch");
+  rc = note_use(d, plan, L->stream);
+  if (rc) return rc;
   e = cudaMemcpyAsync(out.data(), da.out, out.size() * 8, cudaMemcpyDeviceToHost, L->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, da.status, 4, cudaMemcpyDeviceToHost, L->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
@@ -856,7 +967,10 @@ void dvc_shutdown(void) {
     DeviceScratch *d = kv.second;
     cudaSetDevice(d->device);
     cudaDeviceSynchronize();
-    for (auto &p : d->plans) free_plan(p);
+    for (auto &p : d->plans) free_plan_now(p);
+    for (auto &p : d->zombies) free_plan_now(p);
+    for (auto &b : d->pool) cudaFree(b.first);
+    for (auto ev : d->events) cudaEventDestroy(ev);
     if (d->d_counters) cudaFree(d->d_counters);
     for (auto &kv2 : d->lanes) {
       if (kv2.second.d_hist) cudaFree(kv2.second.d_hist);
