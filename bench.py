@@ -244,6 +244,23 @@ def run_reference_sweep(args):
         print(json.dumps({"run": run, "workers": workers, "total_simulations": total, "elapsed_ns": int(t_s * 1e9),
                           "sims_per_sec": total / t_s, "device": "cpu", "kernel": "oracle"}), flush=True)
 
+    if args.ref_sweep == "core1":
+        # SURVEY §8(d) protocol: one process pinned to one core, the first 10^6
+        # playouts of the C2 workload (seed 1, all actions, sims [0, ceil(1e6/A)))
+        per = -(-1000000 // A)
+        try:
+            os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        except (AttributeError, OSError):
+            pass
+        oracle.rollout(d, codes, 1, 0, 0, 1)                          # warm
+        t0 = time.perf_counter()
+        oracle.rollout(d, codes, 1, 0, 0, per)
+        dt = time.perf_counter() - t0
+        print(json.dumps({"run": -1, "workers": 1, "total_simulations": per * A, "elapsed_ns": int(dt * 1e9),
+                          "sims_per_sec": per * A / dt, "device": "cpu", "kernel": "oracle",
+                          "sample": "%s seed 1, %d actions x %d sims, one pinned core" % (WORKLOAD, A, per)}),
+              flush=True)
+        return 0
     if args.ref_sweep == "exp1":
         with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as ex:
             list(ex.map(_oracle_job, [(d, codes, 1, 0, 1)] * cores))          # warm the workers
@@ -437,7 +454,7 @@ def main():
     ap.add_argument("--sims", type=int, default=SIMS_PER_ACTION)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-sweep", choices=["exp1", "exp2"], default=None,
+    ap.add_argument("--ref-sweep", choices=["core1", "exp1", "exp2"], default=None,
                     help="reference arm: the paper's CPU experiment sweeps (tools/paper_experiments.py)")
     ap.add_argument("--ref-sizes", default="1,10,100,1000,10000,100000,1000000")
     args = ap.parse_args()

@@ -94,7 +94,11 @@ def main():
         f.write(hdr)
         for r in rows:
             f.write("%d,%d,%d,%d,%.6e,%s,%s\n" % r)
-    print(json.dumps({"cores": cores}))
+    # ---- the oracle on one pinned core, first 10^6 playouts of C2
+    one = cpu_rows("core1", 1)
+    with open(os.path.join(args.out, "%s_cpu_1core.json" % args.tag), "w") as f:
+        json.dump(one[-1] if one else None, f, indent=1)
+    print(json.dumps({"cores": cores, "one_core": one[-1] if one else None}))
 
 
 if __name__ == "__main__":
