@@ -343,7 +343,8 @@ void fill_kparams(KParams &kp, const State *st, uint64_t seed, uint32_t node_id,
 }
 
 // Core enqueue: adds hist for [sim_begin, sim_end) into d_hist on stream.
-struct PathArg {
+// BatchOpts: a deep-tree forced path (§R9) or the root-batch flags (§R3 CRN, §R10).
+struct BatchOpts {
   const uint32_t *codes = nullptr;
   int32_t len = 0;
   unsigned long long *d_voids = nullptr;
@@ -353,7 +354,7 @@ struct PathArg {
 
 int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed, uint32_t node_id,
             uint64_t sim_begin, uint64_t sim_end, unsigned long long *d_hist, uint8_t *d_winners,
-            int32_t device, cudaStream_t stream, DeviceScratch **dev_out, const PathArg &path = PathArg()) {
+            int32_t device, cudaStream_t stream, DeviceScratch **dev_out, const BatchOpts &path = BatchOpts()) {
   const State *st = as_state(s);
   if (!st) return set_err(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
   if (!actions || n_actions < 1 || n_actions > kMaxActions)
@@ -490,7 +491,7 @@ int flat_search_gpu_impl(const dvc_state *s, const uint32_t *codes, int32_t A, c
       e = cudaMemcpyAsync(L->d_search + off_bp, batch_pos, (size_t)A * 4, cudaMemcpyHostToDevice, L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "search setup");
   }
-  PathArg opt;
+  BatchOpts opt;
   opt.crn = (p->flags & DVC_FLAG_CRN) != 0;
   opt.informed = (p->flags & DVC_FLAG_INFORMED) != 0;
   int rc = enqueue(s, first, k, p->seed, 0u, 0, n, L->d_hist, nullptr, d->device, L->stream, nullptr, opt);
@@ -751,7 +752,7 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
     cudaError_t e = cudaMemsetAsync(L->d_hist, 0, n * sizeof(unsigned long long), L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
   }
-  PathArg opt;
+  BatchOpts opt;
   opt.crn = (flags & DVC_FLAG_CRN) != 0;
   opt.informed = (flags & DVC_FLAG_INFORMED) != 0;
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
@@ -773,7 +774,7 @@ int rollout_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions
   if (!d_hist) return set_err(DVC_E_CONFIG, "d_hist is null");
   if (flags & ~(uint32_t)(DVC_FLAG_CRN | DVC_FLAG_INFORMED)) return set_err(DVC_E_CONFIG, "unknown batch flag");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
-  PathArg opt;
+  BatchOpts opt;
   opt.crn = (flags & DVC_FLAG_CRN) != 0;
   opt.informed = (flags & DVC_FLAG_INFORMED) != 0;
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
@@ -846,7 +847,7 @@ int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_l
     cudaError_t e = cudaMemsetAsync(L->d_hist, 0, (n + n_actions) * sizeof(unsigned long long), L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
   }
-  PathArg pa;
+  BatchOpts pa;
   pa.codes = path;
   pa.len = path_len;
   pa.d_voids = L->d_hist + n;
