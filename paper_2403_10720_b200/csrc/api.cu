@@ -399,7 +399,10 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
 
   const int variant = (int)g_kernel.load();
   const int block = (int)g_block.load();
-  const int mode = kp.path_len > 0 ? kModePath : (path.informed ? kModeInformed : kModePlain);
+  const int mode = kp.path_len > 0 ? kModePath
+                 : path.informed  ? kModeInformed
+                 : d_winners      ? kModeTrace
+                                  : kModePlain;
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
   size_t smem = ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
   if (variant == 0) smem += (size_t)(block / 32) * 64 * (P + 7) * sizeof(uint32_t);

@@ -68,10 +68,12 @@ __device__ __forceinline__ uint32_t outcome(const Sim<P> &S, uint32_t st, const 
   return (st == VOID || S.fi <= kp.path_len) ? (uint32_t)P : winner_seat(S);
 }
 
+// Count a finished playout (and, in the trace mode only, write its winner).
+template <int MODE>
 __device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P, uint32_t a, uint32_t s,
                                        uint32_t w) {
   atomicAdd(&sm.hist[a * (P + 1) + w], 1u);
-  if (kp.winners) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)w;
+  if (MODE == kModeTrace) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)w;
 }
 
 // Start of playout (a, s): determinization block D, table lookup (a2), root
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
     uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, code, meta, kp);
     for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
       st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
-    record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
+    record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
   flush_hist(sm.hist, kp, P);
 }
@@ -186,7 +188,7 @@ struct RingView {
     base[(P + 0) * kRing + i] = S.V;
     base[(P + 1) * kRing + i] = S.Q;
     base[(P + 2) * kRing + i] = S.ji;
-    base[(P + 3) * kRing + i] = S.g | (S.pend << 2) | (S.corr << 8) | (st << 16) | (S.fi << 20);
+    base[(P + 3) * kRing + i] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (S.fi << 28);   // byte fields
     base[(P + 4) * kRing + i] = a;
     base[(P + 5) * kRing + i] = s;
     base[(P + 6) * kRing + i] = code;
@@ -199,11 +201,11 @@ struct RingView {
     S.Q = base[(P + 1) * kRing + i];
     S.ji = base[(P + 2) * kRing + i];
     const uint32_t pk = base[(P + 3) * kRing + i];
-    S.g = pk & 3u;
-    S.pend = (pk >> 2) & 31u;
-    S.corr = (pk >> 8) & 0xFFu;
-    st = (pk >> 16) & 0xFu;
-    S.fi = pk >> 20;
+    S.g = pk & 0xFFu;
+    S.pend = (pk >> 8) & 0xFFu;
+    S.corr = (pk >> 16) & 0xFFu;
+    st = (pk >> 24) & 0xFu;
+    S.fi = pk >> 28;
     a = base[(P + 4) * kRing + i];
     s = base[(P + 5) * kRing + i];
     code = base[(P + 6) * kRing + i];
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       if (valid) {
         pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcode, pmeta, kp);
         if (pst == FINISH) {                    // decided by the root action alone
-          record(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
+          record<MODE>(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
           valid = false;
         }
       }
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
       ++k;
       if (st == FINISH || st == VOID) {
-        record(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
+        record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
         active = false;
       }
     }
@@ -795,6 +797,7 @@ template <int P, bool JOK, bool CONS>
 KernelFn pick_kernel(int variant, int mode) {
   if (mode == kModePath) return pick_mode<P, JOK, CONS, kModePath>(variant);
   if (mode == kModeInformed) return pick_mode<P, JOK, CONS, kModeInformed>(variant);
+  if (mode == kModeTrace) return pick_mode<P, JOK, CONS, kModeTrace>(variant);
   return pick_mode<P, JOK, CONS, kModePlain>(variant);
 }
 

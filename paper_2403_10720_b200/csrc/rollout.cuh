@@ -17,9 +17,10 @@ namespace dvc {
 constexpr int kMaxActions = 768;
 
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
-constexpr uint32_t kCrnWord = 0xFFFFFFFEu;
-// Kernel modes: root batches, deep-tree (forced path) batches, informed policy (§R10).
-constexpr int kModePlain = 0, kModePath = 1, kModeInformed = 2;   // D's counter word z under common random numbers (no action code)
+constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's counter word z under common random numbers (no action code)
+// Kernel modes: root batches, deep-tree (forced path) batches, informed policy
+// (§R10), root batches writing the per-playout winner trace (parity tests).
+constexpr int kModePlain = 0, kModePath = 1, kModeInformed = 2, kModeTrace = 3;
 
 struct KParams {
   uint32_t k0, k1;        // Philox key = (lo32(seed), hi32(seed))
@@ -175,7 +176,7 @@ struct Sim {
 
 template <int P>
 __device__ __forceinline__ bool over(const Sim<P> &S) {
-  if (P == 2) return !(S.H[0] & ~S.V) || !(S.H[1] & ~S.V);
+  if (P == 2) return ((S.H[0] & ~S.V) == 0u) | ((S.H[1] & ~S.V) == 0u);   // no short-circuit branch
   int alive = 0;
 #pragma unroll
   for (int d = 0; d < P; ++d) alive += (S.H[d] & ~S.V) ? 1 : 0;
@@ -184,6 +185,7 @@ __device__ __forceinline__ bool over(const Sim<P> &S) {
 
 template <int P>
 __device__ __forceinline__ uint32_t winner_seat(const Sim<P> &S) {
+  if (P == 2) return S.g ^ ((S.H[0] & ~S.V) ? 0u : 1u);      // the mover, else the other seat
   uint32_t d = 0;
 #pragma unroll
   for (int i = P - 1; i >= 1; --i) d = (S.H[i] & ~S.V) ? (uint32_t)i : d;
