@@ -179,38 +179,55 @@ constexpr uint32_t kRing = 64;
 
 template <int P>
 struct RingView {
-  uint32_t *base;   // SoA: field f of slot i at base[f * kRing + i]
-  static constexpr int kFields = P + 7;   // H[P], V, Q, ji, packed(g|pend|corr|st), a, s, code
+  // AoS, 48 B per slot (three 16 B vectors): a pop is 3 LDS.128 -- pops run
+  // in a divergent region with ~2 lanes, so instructions, not bank
+  // conflicts, are what they cost.  Words: H[P], V, Q, ji, packed
+  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, code.
+  uint4 *base;
   __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
                                       uint32_t code) const {
+    uint32_t w[12];
 #pragma unroll
-    for (int d = 0; d < P; ++d) base[d * kRing + i] = S.H[d];
-    base[(P + 0) * kRing + i] = S.V;
-    base[(P + 1) * kRing + i] = S.Q;
-    base[(P + 2) * kRing + i] = S.ji;
-    base[(P + 3) * kRing + i] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (S.fi << 28);   // byte fields
-    base[(P + 4) * kRing + i] = a;
-    base[(P + 5) * kRing + i] = s;
-    base[(P + 6) * kRing + i] = code;
+    for (int d = 0; d < P; ++d) w[d] = S.H[d];
+    w[P + 0] = S.V;
+    w[P + 1] = S.Q;
+    w[P + 2] = S.ji;
+    w[P + 3] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (S.fi << 28);
+    w[P + 4] = a;
+    w[P + 5] = s;
+    w[P + 6] = code;
+#pragma unroll
+    for (int j = P + 7; j < 12; ++j) w[j] = 0;
+    base[3 * i + 0] = make_uint4(w[0], w[1], w[2], w[3]);
+    base[3 * i + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    if (P + 7 > 8) base[3 * i + 2] = make_uint4(w[8], w[9], w[10], w[11]);
   }
   __device__ __forceinline__ void get(uint32_t i, Sim<P> &S, uint32_t &st, uint32_t &a, uint32_t &s,
                                       uint32_t &code) const {
+    const uint4 q0 = base[3 * i + 0], q1 = base[3 * i + 1];
+    const uint4 q2 = (P + 7 > 8) ? base[3 * i + 2] : make_uint4(0, 0, 0, 0);
+    const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
 #pragma unroll
-    for (int d = 0; d < P; ++d) S.H[d] = base[d * kRing + i];
-    S.V = base[(P + 0) * kRing + i];
-    S.Q = base[(P + 1) * kRing + i];
-    S.ji = base[(P + 2) * kRing + i];
-    const uint32_t pk = base[(P + 3) * kRing + i];
+    for (int d = 0; d < P; ++d) S.H[d] = w[d];
+    S.V = w[P + 0];
+    S.Q = w[P + 1];
+    S.ji = w[P + 2];
+    const uint32_t pk = w[P + 3];
     S.g = pk & 0xFFu;
     S.pend = (pk >> 8) & 0xFFu;
     S.corr = (pk >> 16) & 0xFFu;
     st = (pk >> 24) & 0xFu;
     S.fi = pk >> 28;
-    a = base[(P + 4) * kRing + i];
-    s = base[(P + 5) * kRing + i];
-    code = base[(P + 6) * kRing + i];
+    a = w[P + 4];
+    s = w[P + 5];
+    code = w[P + 6];
   }
 };
+
+// First 16 B-aligned word of the refill kernel's rings in dynamic smem.
+__host__ __device__ __forceinline__ uint32_t ring_word_offset(uint32_t A, int P) {
+  return (A * (uint32_t)(P + 3) + (uint32_t)kMaxPath + 3u) & ~3u;
+}
 
 template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_constant__ KParams kp) {
@@ -219,7 +236,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{sh_all + kp.A * (P + 3) + kMaxPath + (threadIdx.x >> 5) * RingView<P>::kFields * kRing};
+  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * 3 * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
   // slices of ONE action, so no per-lane division).  The next batch index is
   // claimed one batch ahead (lane 0's atomicAdd result is only read at the
