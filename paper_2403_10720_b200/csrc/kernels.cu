@@ -135,7 +135,8 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
   dbg_check_state<P, JOK>(S, kp);
   return r;
 #else
-  return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
+  if (PATH) return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
+  return finish_decision<P, JOK, CONS>(S, stop, t, correct, kp);
 #endif
 }
 

@@ -326,6 +326,22 @@ __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct,
   return over(S) ? FINISH : cont;
 }
 
+// The end of a decision step without a branch on STOP: a STOP (stop = true)
+// reveals nothing and ends the turn, any guess resolves as above.  Lanes that
+// stop and lanes that guess run the same instructions (no divergent region).
+template <int P, bool JOK, bool CONS>
+__device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32_t t, bool correct,
+                                                    const KParams &kp) {
+  const bool pend_hidden = S.pend != kNoKey && !((S.V >> S.pend) & 1u);
+  const uint32_t lmh = leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
+  const uint32_t r = correct ? t : (pend_hidden ? S.pend : lmh);
+  S.V |= stop ? 0u : (1u << (r & 31u));
+  const bool hit = correct && !stop;
+  S.corr += hit ? 1u : 0u;
+  const uint32_t cont = (CONS && hit) ? DECIDE : END_TURN;
+  return (!stop && over(S)) ? FINISH : cont;
+}
+
 // Hidden tile of opponent hand Hd selected by index x of the mover's LEGAL
 // list restricted to Hd (slots in line order, nB / nW values per black / white
 // slot); returns the tile and the value index inside the slot.
