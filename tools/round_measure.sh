@@ -5,8 +5,6 @@ TAG=${1:-r01}
 O=gpurun_out/$TAG
 mkdir -p $O
 set -x
-python bench.py > $O/bench.jsonl 2> $O/bench.err
-python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.jsonl 2> $O/bench_ref.err
 python tools/configs_bench.py > $O/configs.jsonl 2> $O/configs.err
 python tools/c5_sweep.py --out $O --tag $TAG > $O/c5.log 2>&1
 python tools/paper_experiments.py --out $O --tag $TAG > $O/exp.log 2>&1
@@ -24,4 +22,8 @@ python tools/profile_run.py --launches 2 --kernel naive --block 1024 > $O/p2.log
 python tools/profile_run.py --launches 2 --workload fixtures/c4_d1.json --sims 100000 > $O/p3.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:rollout_refill -s 1 -c 1 -o $O/refill_c4 \
       python tools/profile_run.py --launches 2 --workload fixtures/c4_d1.json --sims 100000 > /dev/null 2>&1
+# the bench line last, with the per-playout instruction count of the capture above
+python tools/summarize_profile.py $O/refill_c2.ncu-rep 21000000 $O/refill_c2_summary.json --unit > /dev/null
+python bench.py > $O/bench.jsonl 2> $O/bench.err
+python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.jsonl 2> $O/bench_ref.err
 echo done
