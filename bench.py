@@ -37,7 +37,8 @@ METRIC = "playouts/sec (1/2/4/8 B200) and warp exec efficiency vs CPU oracle"
 UNIT = "playouts/s"
 
 
-def load_workload(path=WORKLOAD):
+def load_workload(path=None):
+    path = path or WORKLOAD
     with open(os.path.join(ROOT, path)) as f:
         return json.load(f)
 
@@ -457,7 +458,12 @@ def main():
     ap.add_argument("--ref-sweep", choices=["core1", "exp1", "exp2"], default=None,
                     help="reference arm: the paper's CPU experiment sweeps (tools/paper_experiments.py)")
     ap.add_argument("--ref-sizes", default="1,10,100,1000,10000,100000,1000000")
+    ap.add_argument("--workload", default=None,
+                    help="experiments only: another fixture for the timed batch (the bench line is C2)")
     args = ap.parse_args()
+    if args.workload:
+        global WORKLOAD
+        WORKLOAD = args.workload
     if args.impl == "reference":
         return run_reference_sweep(args) if args.ref_sweep else run_reference(args)
     return run_product(args)

@@ -206,7 +206,8 @@ __device__ __forceinline__ uint32_t kap_w(uint32_t ji) { return (ji >> 5) & 31u;
 __device__ __forceinline__ bool joker_first(uint32_t ji, uint32_t other_is_w, uint32_t k_other,
                                             uint32_t k_j) {
   const bool wfirst = (ji >> 10) & 1u;
-  return k_other < k_j || (k_other == k_j && (other_is_w ? wfirst : !wfirst));
+  // bitwise, not short-circuit: no divergent branch
+  return (k_other < k_j) | ((k_other == k_j) & (other_is_w ? wfirst : !wfirst));
 }
 
 // Leftmost hidden tile of hand Hp (DESIGN.md §R5 APPLY).
@@ -218,14 +219,14 @@ __device__ __forceinline__ uint32_t leftmost_hidden(uint32_t Hp, uint32_t V, uin
   const uint32_t kmin = __ffs(hn) - 1u;
   if (!JOK) return kmin;
   const uint32_t hj = (hid >> kp.JB) & 3u;
-  if (!hj) return kmin;
-  // a hidden joker precedes the lowest hidden numbered tile iff kappa <= its key
+  // a hidden joker precedes the lowest hidden numbered tile iff kappa <= its
+  // key; computed for every lane (no branch on "holds a hidden joker")
   const uint32_t lim = hn ? kmin : 32u;
   const uint32_t kb = kap_b(ji), kw = kap_w(ji);
-  const bool cb = (hj & 1u) && kb <= lim;
-  const bool cw = (hj & 2u) && kw <= lim;
-  if (cb && cw) return joker_first(ji, 1u, kw, kb) ? kp.JB + 1 : kp.JB;
-  return cb ? kp.JB : (cw ? kp.JB + 1 : kmin);
+  const bool cb = (hj & 1u) & (kb <= lim);
+  const bool cw = ((hj >> 1) & 1u) & (kw <= lim);
+  const uint32_t both = joker_first(ji, 1u, kw, kb) ? kp.JB + 1 : kp.JB;
+  return (cb & cw) ? both : (cb ? kp.JB : (cw ? kp.JB + 1 : kmin));
 }
 
 // 0-based line position of key v held in hand Hp (root action, §R1 "position").
@@ -368,7 +369,7 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
       uint32_t c = nB * __popc(hb & pre) + nW * __popc(hw & pre);
       const bool hidO = is_w ? hidB : hidW;
       const uint32_t ko = is_w ? kb : kw;
-      c += (hidO && joker_first(ji, is_w ^ 1u, ko, kj)) ? (is_w ? nB : nW) : 0u;
+      c += (hidO & joker_first(ji, is_w ^ 1u, ko, kj)) ? (is_w ? nB : nW) : 0u;
       const uint32_t nJ = is_w ? nW : nB;
       const bool here = hidJ && x >= c && x < c + nJ;
       sel = here ? kp.JB + is_w : sel;
