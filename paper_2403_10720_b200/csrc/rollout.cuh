@@ -263,16 +263,17 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t wx, uint
 #pragma unroll
     for (int d = P - 2; d >= 1; --d) delta = (S.H[d] & ~S.V) ? (uint32_t)d : delta;
     delta = et ? delta : 0u;
-    uint32_t Hn[P];
+    // rotate the hands by delta (< 4) as a rotation by 1 if bit 0, then by 2
+    // if bit 1: 2P selects instead of P(P-1)
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-      uint32_t v = S.H[i];
+    for (int sh = 1; sh <= 2; sh <<= 1) {
+      const bool c = (delta & (uint32_t)sh) != 0u;
+      uint32_t Hn[P];
 #pragma unroll
-      for (int dd = 1; dd < P; ++dd) v = (delta == (uint32_t)dd) ? S.H[(i + dd) % P] : v;
-      Hn[i] = v;
+      for (int i = 0; i < P; ++i) Hn[i] = c ? S.H[(i + sh) % P] : S.H[i];
+#pragma unroll
+      for (int i = 0; i < P; ++i) S.H[i] = Hn[i];
     }
-#pragma unroll
-    for (int i = 0; i < P; ++i) S.H[i] = Hn[i];
     S.g += delta;
     S.g = S.g >= (uint32_t)P ? S.g - P : S.g;
   }
