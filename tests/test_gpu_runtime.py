@@ -57,6 +57,28 @@ def test_concurrent_streams(dvc):
             assert (h.cpu().numpy().astype(np.uint64) == r).all()
 
 
+def test_eviction_while_launches_in_flight(dvc):
+    """More distinct states than the plan cache holds, launched asynchronously
+    on four streams without synchronising: evicted plans must stay intact
+    until every launch reading them has finished (per-stream use events and
+    the zombie list), and their buffers are reused only then.  Every result
+    equals the same batch run alone."""
+    ds = [json.load(open(p)) for p in FIX[:48]]
+    sts = [dvc.encode(d) for d in ds]
+    codes = [st.legal_actions()[:4] for st in sts]
+    ref = [dvc.rollout_batch_ex(st, c, 9, 0, 0, 3000) for st, c in zip(sts, codes)]
+    dvc.shutdown()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    hists = [torch.zeros((len(c), st.players), dtype=torch.int64, device="cuda") for st, c in zip(sts, codes)]
+    torch.cuda.synchronize()
+    for rep in range(2):
+        for i, (st, c, h) in enumerate(zip(sts, codes, hists)):
+            dvc.rollout_batch_async(st, c, 9, 0, 0, 3000, h, stream=streams[i % 4])
+        torch.cuda.synchronize()
+        for h, r in zip(hists, ref):
+            assert (h.cpu().numpy().astype(np.uint64) == (rep + 1) * r).all()
+
+
 def test_table_cap_boundary(dvc):
     d = json.load(open(os.path.join(ROOT, "fixtures", "c1_d5.json")))
     st = dvc.encode(d)
