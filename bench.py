@@ -418,6 +418,10 @@ def run_product(args):
             roof["frac"] = roof["achieved"] / peak
             roof["per_unit"] = "%.0f thread-instructions per playout (%s)" % (ipp, unit.get("source", ""))
             roof["traffic"] = unit.get("dram_bytes_per_launch")
+            # the same capture's view of the binding unit: the ALU pipe runs at
+            # half the issue rate (LOP3/SHF/ISETP/SEL..., 16 lanes/clk/SMSP)
+            roof["ncu"] = {k: unit.get(k) for k in ("eta_simt", "issue_active_pct", "pipe_alu_pct", "pipe_xu_pct",
+                                                    "pipe_fma_pct")}
         else:
             roof["achieved"] = None
             roof["frac"] = None

@@ -84,7 +84,8 @@ def main():
                 "thread_inst_per_playout": res["thread_inst_per_playout"],
                 "dram_bytes_per_launch": res["dram_bytes_per_launch"],
                 "eta_simt": res["eta_simt"], "issue_active_pct": res["issue_active_pct"],
-                "source": out}
+                "pipe_alu_pct": res.get("pipe_alu_pct"), "pipe_xu_pct": res.get("pipe_xu_pct"),
+                "pipe_fma_pct": res.get("pipe_fma_pct"), "source": out}
         with open("profiles/roofline_unit.json", "w") as f:
             json.dump(unit, f, indent=1)
 
