@@ -22,6 +22,10 @@
 
 namespace dvc {
 
+#ifndef DVC_REFILL_MINB
+#define DVC_REFILL_MINB 3   // min resident 256-thread blocks per SM (register cap)
+#endif
+
 constexpr uint32_t kBatch = 32;   // sims per work batch of the refill kernel (one produce round)
 
 // Shared memory: hist[A*P] u32 counters, then the action codes and metas
@@ -176,17 +180,18 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
 // iteration, so lanes never idle on playout-length variance and the start
 // code never runs with a handful of lanes (BASELINE.json north_star: lanes
 // retire via __ballot_sync and pull new playouts from a work counter).
-constexpr uint32_t kRing = 64;
+constexpr uint32_t kRing = kRingSlots;
 
 template <int P>
 struct RingView {
-  // AoS, 48 B per slot (three 16 B vectors): a pop is 3 LDS.128 -- pops run
-  // in a divergent region with ~2 lanes, so instructions, not bank
-  // conflicts, are what they cost.  Words: H[P], V, Q, ji, packed
-  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, code.
+  // AoS, kRingVecs x 16 B per slot: a pop is 3-4 LDS.128 -- pops run in a
+  // divergent region with ~2 lanes, so instructions, not bank conflicts, are
+  // what they cost.  Words: H[P], V, Q, ji, packed
+  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, code, then
+  // (DVC_PREFETCH_B) the playout's first step block B_0.
   uint4 *base;
   __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
-                                      uint32_t code) const {
+                                      uint32_t code, uint4 B0) const {
     uint32_t w[12];
 #pragma unroll
     for (int d = 0; d < P; ++d) w[d] = S.H[d];
@@ -199,14 +204,18 @@ struct RingView {
     w[P + 6] = code;
 #pragma unroll
     for (int j = P + 7; j < 12; ++j) w[j] = 0;
-    base[3 * i + 0] = make_uint4(w[0], w[1], w[2], w[3]);
-    base[3 * i + 1] = make_uint4(w[4], w[5], w[6], w[7]);
-    if (P + 7 > 8) base[3 * i + 2] = make_uint4(w[8], w[9], w[10], w[11]);
+    uint4 *b = base + kRingVecs * i;
+    b[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    b[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    if (P + 7 > 8) b[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    if (kRingVecs == 4) b[3] = B0;
   }
   __device__ __forceinline__ void get(uint32_t i, Sim<P> &S, uint32_t &st, uint32_t &a, uint32_t &s,
-                                      uint32_t &code) const {
-    const uint4 q0 = base[3 * i + 0], q1 = base[3 * i + 1];
-    const uint4 q2 = (P + 7 > 8) ? base[3 * i + 2] : make_uint4(0, 0, 0, 0);
+                                      uint32_t &code, uint4 &B0) const {
+    const uint4 *b = base + kRingVecs * i;
+    const uint4 q0 = b[0], q1 = b[1];
+    const uint4 q2 = (P + 7 > 8) ? b[2] : make_uint4(0, 0, 0, 0);
+    if (kRingVecs == 4) B0 = b[3];
     const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
 #pragma unroll
     for (int d = 0; d < P; ++d) S.H[d] = w[d];
@@ -231,13 +240,13 @@ __host__ __device__ __forceinline__ uint32_t ring_word_offset(uint32_t A, int P)
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
-__global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(256, DVC_REFILL_MINB) rollout_refill_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
   const Smem sm = setup_smem(kp, P);
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * 3 * kRing};
+  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * kRingVecs * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
   // slices of ONE action, so no per-lane division).  The next batch index is
   // claimed one batch ahead (lane 0's atomicAdd result is only read at the
@@ -250,6 +259,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
   uint32_t head = 0, count = 0;       // ring (warp-uniform)
   bool active = false;
   uint32_t a = 0, s = 0, code = 0, st = FINISH, k = 0;
+  uint4 B = make_uint4(0, 0, 0, 0);   // DVC_PREFETCH_B: the running playout's block for step k
   Sim<P> S;
   while (true) {
     // ---- produce: the whole warp starts up to 32 playouts
@@ -286,7 +296,9 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       }
       Sim<P> T;
       uint32_t pst = FINISH;
+      uint4 B0 = make_uint4(0, 0, 0, 0);
       if (valid) {
+        if (DVC_PREFETCH_B) B0 = philox_rk(0u, ps, pcode, kp.node, kp);
         pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcode, pmeta, kp);
         if (pst == FINISH) {                    // decided by the root action alone
           record<MODE>(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
@@ -294,13 +306,19 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
         }
       }
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, valid);
-      if (valid) ring.put((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcode);
+      if (valid) ring.put((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcode, B0);
       count += __popc(m);
       __syncwarp();
     }
     // ---- one decision step for every running lane
     if (active) {
-      st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
+      if (DVC_PREFETCH_B) {
+        const uint4 Bn = philox_rk(k + 1u, s, code, kp.node, kp);   // next step's block, independent chain
+        st = step_block<P, JOK, CONS, MODE>(S, st, B, k, sm.meta, sm.path, a, kp, kp.path_len);
+        B = Bn;
+      } else {
+        st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
+      }
       ++k;
       if (st == FINISH || st == VOID) {
         record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(256, 3) rollout_refill_kernel(const __grid_con
       if (take) {
         const uint32_t rank = __popc(need & lt_mask);
         if (!active && rank < take) {
-          ring.get((head + rank) & (kRing - 1u), S, st, a, s, code);
+          ring.get((head + rank) & (kRing - 1u), S, st, a, s, code, B);
           k = 0;
           active = true;
         }

@@ -16,6 +16,16 @@ namespace dvc {
 
 constexpr int kMaxActions = 768;
 
+// Refill kernel (kernels.cu): the Philox block of a playout's NEXT decision
+// step is generated during the current one (an independent dependency chain
+// for the scheduler to interleave with the step's serial game logic), so a
+// started playout carries its first step block B_0 in its ring slot.
+#ifndef DVC_PREFETCH_B
+#define DVC_PREFETCH_B 0   // measured: -7% on C2, -3% on C4 (more Philox work, bigger ring slots)
+#endif
+constexpr uint32_t kRingSlots = 64;                          // started playouts per warp
+constexpr uint32_t kRingVecs = DVC_PREFETCH_B ? 4u : 3u;     // 16 B vectors per ring slot
+
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
 constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's counter word z under common random numbers (no action code)
 // Kernel modes: root batches, deep-tree (forced path) batches, informed policy
@@ -143,15 +153,47 @@ __device__ __forceinline__ uint32_t div_per(uint32_t item, const KParams &kp) {
 // ----------------------------------------------------------------- bit helpers
 __device__ __forceinline__ uint32_t below(uint32_t k) { return (1u << k) - 1u; }  // k <= 31
 
+// One probe of the 5-step searches on nk = -k: k += b when
+// popc(m & below(k + b)) <= n.  Written in PTX so the compiler keeps this
+// form: the bits below the probe are counted as popc(m << (32 - b + nk))
+// (one shift, where a mask takes a shift and an AND), and both the shift
+// amount and the accept are immediate adds (VIADD, off the ALU pipe; the
+// accept predicated, not a SEL) -- the ALU pipe is the bench kernel's binding
+// unit.
+template <uint32_t B>
+__device__ __forceinline__ void probe(uint32_t &nk, uint32_t m, uint32_t n) {
+  asm("{\n\t.reg .u32 sh, x;\n\t.reg .pred q;\n\t"
+      "add.u32 sh, %0, %3;\n\tshl.b32 x, %1, sh;\n\tpopc.b32 x, x;\n\t"
+      "setp.le.u32 q, x, %2;\n\t@q sub.u32 %0, %0, %4;\n\t}"
+      : "+r"(nk) : "r"(m), "r"(n), "n"(32 - B), "n"(B));
+}
+
+// The weighted probe of select_slot (same form): black slots weigh nB, white
+// nW; on accept also base = the weight below the probe.
+template <uint32_t B>
+__device__ __forceinline__ void probe_w(uint32_t &nk, uint32_t &base, uint32_t hB, uint32_t hW, uint32_t nB,
+                                        uint32_t nW, uint32_t x) {
+  asm("{\n\t.reg .u32 sh, xb, xw, c;\n\t.reg .pred q;\n\t"
+      "add.u32 sh, %0, %7;\n\tshl.b32 xb, %2, sh;\n\tshl.b32 xw, %3, sh;\n\t"
+      "popc.b32 xb, xb;\n\tpopc.b32 xw, xw;\n\tmul.lo.u32 c, xb, %4;\n\tmad.lo.u32 c, xw, %5, c;\n\t"
+      "setp.le.u32 q, c, %6;\n\t@q sub.u32 %0, %0, %8;\n\t@q mov.u32 %1, c;\n\t}"
+      : "+r"(nk), "+r"(base) : "r"(hB), "r"(hW), "r"(nB), "r"(nW), "r"(x), "n"(32 - B), "n"(B));
+}
+
 // 0-based n-th set bit of m (must exist): fixed 5-step search, no divergence.
 __device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t n) {
-  uint32_t k = 0;
-#pragma unroll
-  for (uint32_t b = 16; b; b >>= 1) {
-    const uint32_t kk = k | b;
-    if ((uint32_t)__popc(m & below(kk)) <= n) k = kk;
-  }
-  return k;
+  uint32_t nk = 0;
+  probe<16>(nk, m, n);
+  probe<8>(nk, m, n);
+  probe<4>(nk, m, n);
+  probe<2>(nk, m, n);
+  probe<1>(nk, m, n);
+  return 0u - nk;
+}
+
+// popc(m & below(t)) for t in [0, 31] as one clamped funnel shift (t = 0 -> 0).
+__device__ __forceinline__ uint32_t popc_below(uint32_t m, uint32_t t) {
+  return (uint32_t)__popc(__funnelshift_lc(0u, m, 32u - t));
 }
 
 template <int P>
@@ -380,14 +422,13 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
     xs = x - sub;
   }
   const uint32_t hB = hid & kp.numm & kEven, hW = hid & kp.numm & kOdd;
-  uint32_t k = 0, base = 0;
-#pragma unroll
-  for (uint32_t b = 16; b; b >>= 1) {
-    const uint32_t kk = k | b;
-    const uint32_t m = below(kk);
-    const uint32_t c = nB * __popc(hB & m) + nW * __popc(hW & m);
-    if (c <= xs) { k = kk; base = c; }
-  }
+  uint32_t nk = 0, base = 0;        // nk = -k, probes as in nth_bit
+  probe_w<16>(nk, base, hB, hW, nB, nW, xs);
+  probe_w<8>(nk, base, hB, hW, nB, nW, xs);
+  probe_w<4>(nk, base, hB, hW, nB, nW, xs);
+  probe_w<2>(nk, base, hB, hW, nB, nW, xs);
+  probe_w<1>(nk, base, hB, hW, nB, nW, xs);
+  const uint32_t k = 0u - nk;
   const bool jok = JOK && sel != kNoKey;
   *t_out = jok ? sel : k;
   *vidx_out = jok ? vidx_j : xs - base;
@@ -430,7 +471,7 @@ __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t wz, const KPara
   uint32_t t, vidx;
   select_slot<JOK>(Hd, S.V, S.ji, nB, nW, x, kp, &t, &vidx);
   *t_out = t;
-  *correct = vidx == (uint32_t)__popc(((t & 1u) ? aW : aB) & below(t));
+  *correct = vidx == popc_below((t & 1u) ? aW : aB, t);
   return stop;
 }
 
