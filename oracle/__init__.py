@@ -3,7 +3,8 @@
 Plain, slow, obviously-correct CPU implementations of what the batched Da Vinci
 Code rollout computes:
 
-  * oracle/philox.py  -- Philox4x32-10, choose, rank64 (the RNG contract);
+  * oracle/philox.py  -- Philox2x32-10, stream key, counter layout, choose,
+                         rank64 (the RNG contract);
   * oracle/game.py    -- list-based rules, canonical determinization
                          (count + unrank) and the Philox-driven playout (Python);
   * oracle/exact.py   -- exact rational win probabilities (tiny tile sets);
@@ -48,7 +49,10 @@ def lib():
         L = ctypes.CDLL(_SO)
         P, U32, U64, I32 = ctypes.POINTER, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
         L.oracle_last_error.restype = ctypes.c_char_p
-        L.oracle_philox.argtypes = [P(U32), P(U32), P(U32)]
+        L.oracle_philox2.argtypes = [P(U32), U32, P(U32)]
+        L.oracle_stream_key.argtypes = [U64, U32]
+        L.oracle_stream_key.restype = U32
+        L.oracle_step_block.argtypes = [U64, U32, U32, U32, U32, P(U32)]
         L.oracle_count.argtypes = [P(I32), P(U64)]
         L.oracle_unrank.argtypes = [P(I32), U64, P(I32), I32, P(I32)]
         L.oracle_legal.argtypes = [P(I32), P(U32), I32, P(I32)]
@@ -83,11 +87,22 @@ def _check(rc):
     return rc
 
 
-def philox_block(ctr, key):
-    c = (ctypes.c_uint32 * 4)(*ctr)
-    k = (ctypes.c_uint32 * 2)(*key)
-    o = (ctypes.c_uint32 * 4)()
-    lib().oracle_philox(c, k, o)
+def philox2(ctr, key):
+    """Philox2x32-10 of the C++ oracle: ctr 2 x u32, key u32 -> 2 x u32."""
+    c = (ctypes.c_uint32 * 2)(*ctr)
+    o = (ctypes.c_uint32 * 2)()
+    lib().oracle_philox2(c, key, o)
+    return tuple(o)
+
+
+def stream_key(seed, node_id):
+    return lib().oracle_stream_key(seed, node_id)
+
+
+def step_block(seed, node_id, code, s, t):
+    """B_t (t = 63: the determinization block D) of the C++ oracle."""
+    o = (ctypes.c_uint32 * 2)()
+    lib().oracle_step_block(seed, node_id, code, s, t, o)
     return tuple(o)
 
 

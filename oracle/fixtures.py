@@ -42,7 +42,7 @@ def _deal(rules, per, rng):
 
 def _start_turn(game, rng, first=False):
     if not first:
-        game.start_turn(rng.getrandbits(32), rng.getrandbits(32))
+        game.start_turn(rng.getrandbits(32), gap_word=rng.getrandbits(32))
     else:  # seat 0's first turn: draw without advancing the mover
         game.pend, game.corr = NONE, 0
         if game.pool:

@@ -255,15 +255,19 @@ class Game:
                 return p
         raise AssertionError
 
-    def start_turn(self, wx, wy):
-        """END_TURN handling: next alive player, draw with words (wx, wy)."""
+    def start_turn(self, w, gap_word=None):
+        """END_TURN handling: next alive player, draw with word w = b0 (§R3):
+        pool index choose(|Q|, w); a drawn joker's gap from the remainder.
+        (gap_word: the fixture generator's own second word, not the contract.)"""
         self.g = self.next_mover()
         self.pend = NONE
         self.corr = 0
         if self.pool:
-            t = self.pool.pop(px.choose(len(self.pool), wx))
+            q = len(self.pool)
+            t = self.pool.pop(px.choose(q, w))
             if self.rules.is_joker(t):
-                gap = px.choose(len(self.lines[self.g]) + 1, wy)
+                gw = px.remainder(q, w) if gap_word is None else gap_word
+                gap = px.choose(len(self.lines[self.g]) + 1, gw)
                 self.insert_joker(self.g, t, gap)
             else:
                 self.insert_numbered(self.g, t)
@@ -472,7 +476,8 @@ class DetSpace:
 
 def playout(space, code, seed, node_id, s, trace=None, crn=False, informed=False):
     """One playout: determinize with block D, apply the root action, then play
-    uniformly random decisions with one Philox block per decision step.
+    uniformly random decisions with one Philox2x32 block per decision step
+    (b0: draw, b1: decision; §R3).
     Returns the winner seat.  crn: D is keyed by CRN_WORD instead of the code
     (common determinizations across actions); informed: every
     decision is uniform over the order-aware list (§R10) instead of LEGAL."""
@@ -489,10 +494,10 @@ def playout(space, code, seed, node_id, s, trace=None, crn=False, informed=False
             return w
         B = px.step_block(seed, node_id, code, s, k)
         if step == "END_TURN":
-            game.start_turn(B[0], B[1])
+            game.start_turn(B[0])
         L = game.legal(informed)
         n = game.n_choices(L)
-        i = px.choose(n, B[2])
+        i = px.choose(n, B[1])
         k += 1
         a = STOP if i == len(L) else L[i]
         if trace is not None:
@@ -524,7 +529,7 @@ def playout_path(space, path, code, seed, node_id, s, trace=None):
             return VOID if fi < len(F) else game.winner()
         B = px.step_block(seed, node_id, code, s, k)
         if step == "END_TURN":
-            game.start_turn(B[0], B[1])
+            game.start_turn(B[0])
         L = game.legal()
         n = game.n_choices(L)
         if fi < len(F) and game.g == viewer:
@@ -534,7 +539,7 @@ def playout_path(space, path, code, seed, node_id, s, trace=None):
             if a not in allowed:
                 return VOID
         else:
-            i = px.choose(n, B[2])
+            i = px.choose(n, B[1])
             a = STOP if i == len(L) else L[i]
         k += 1
         if trace is not None:

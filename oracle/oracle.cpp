@@ -25,27 +25,42 @@ namespace {
 typedef uint32_t u32;
 typedef uint64_t u64;
 
-const u32 STOP = 0xFFFFFFFFu;
 const int NONE = -1;
 
 // ------------------------------------------------------------------ Philox (§R3)
-struct Block { u32 v[4]; };
+// Philox2x32-10 (Salmon et al. SC'11; Random123 philox2x32).
+struct Block { u32 v[2]; };
 
-Block philox(u32 c0, u32 c1, u32 c2, u32 c3, u32 k0, u32 k1) {
+Block philox2(u32 c0, u32 c1, u32 k) {
   for (int r = 0; r < 10; ++r) {
-    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
-    u64 p0 = (u64)0xD2511F53u * c0;
-    u64 p1 = (u64)0xCD9E8D57u * c2;
-    u32 hi0 = (u32)(p0 >> 32), lo0 = (u32)p0;
-    u32 hi1 = (u32)(p1 >> 32), lo1 = (u32)p1;
-    u32 n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
-    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    if (r > 0) k += 0x9E3779B9u;
+    u64 p = (u64)0xD256D193u * c0;
+    u32 hi = (u32)(p >> 32), lo = (u32)p;
+    u32 n0 = hi ^ k ^ c1, n1 = lo;
+    c0 = n0; c1 = n1;
   }
-  Block b; b.v[0] = c0; b.v[1] = c1; b.v[2] = c2; b.v[3] = c3;
+  Block b; b.v[0] = c0; b.v[1] = c1;
   return b;
 }
 
+const u32 STOP = 0xFFFFFFFFu;
+const u32 CRN_WORD = 0xFFFFFFFEu;
+
+// stream key K(seed, node) = word 0 of Philox2x32-10((lo32(seed), hi32(seed)), node)
+u32 stream_key(u64 seed, u32 node) { return philox2((u32)seed, (u32)(seed >> 32), node).v[0]; }
+
+// 12-bit image of an action code: target<<10 | position<<5 | value; STOP 0xFFF; CRN 0xFFE
+u32 code12(u32 code) {
+  if (code == STOP) return 0xFFFu;
+  if (code == CRN_WORD) return 0xFFEu;
+  return ((code >> 24) << 10) | (((code >> 16) & 0xFFu) << 5) | (code & 0xFFFFu);
+}
+
+// counter word c1 = t | code12 << 6 | (node mod 2^14) << 18; t = 63 for D
+u32 ctr1(u32 t, u32 code, u32 node) { return t | (code12(code) << 6) | ((node & 0x3FFFu) << 18); }
+
 u32 choose(u32 n, u32 w) { return (u32)(((u64)w * n) >> 32); }
+u32 remainder(u32 n, u32 w) { return (u32)((u64)w * n); }   // the word left over by choose
 
 u64 rank64(u64 N, u32 w0, u32 w1) {
   unsigned __int128 x = (((unsigned __int128)w1) << 32) | w0;
@@ -171,16 +186,19 @@ struct Game {
     lines[g][idx].rev = true;
     return over() ? FINISH : END_TURN;
   }
-  void start_turn(u32 wx, u32 wy) {
+  // draw word w = b0: pool index choose(|Q|, w); a drawn joker's gap from
+  // the remainder (w * |Q|) mod 2^32 (§R3)
+  void start_turn(u32 w) {
     int P = rules.P, nxt = -1;
     for (int d = 1; d <= P; ++d) { int p = (g + d) % P; if (alive(p)) { nxt = p; break; } }
     g = nxt; pend = NONE; corr = 0;
     if (!pool.empty()) {
-      u32 i = choose((u32)pool.size(), wx);
+      const u32 q = (u32)pool.size();
+      u32 i = choose(q, w);
       int t = pool[i];
       pool.erase(pool.begin() + i);
       if (is_joker(rules, t)) {
-        u32 gap = choose((u32)lines[g].size() + 1, wy);
+        u32 gap = choose((u32)lines[g].size() + 1, remainder(q, w));
         lines[g].insert(lines[g].begin() + gap, Tile{t, false});
       } else {
         insert_numbered(g, t);
@@ -376,22 +394,22 @@ void root_legal(const Obs &o, std::vector<u32> &out) {
 // Philox block per decision step.  Returns the winner; *steps = #decisions.
 // crn: D keyed by CRN_WORD instead of the code (common determinizations
 // across actions).
-const u32 CRN_WORD = 0xFFFFFFFEu;
 
 int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
             std::vector<u32> &L, bool crn = false, bool informed = false) {
-  u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
-  Block D = philox(0xFFFFFFFFu, s, crn ? CRN_WORD : code, node, k0, k1);
+  const u32 K = stream_key(seed, node);
+  Block D = philox2(s, ctr1(63, crn ? CRN_WORD : code, node), K);
   u64 rho = rank64(sp.N, D.v[0], D.v[1]);
   Game G = sp.game(sp.unrank(rho));
   Game::Step st = G.apply(code);
   u32 k = 0;
   while (st != Game::FINISH) {
-    Block B = philox(k, s, code, node, k0, k1);
-    if (st == Game::END_TURN) G.start_turn(B.v[0], B.v[1]);
+    if (k > 62) throw std::runtime_error("more than 63 decisions in one playout");
+    Block B = philox2(s, ctr1(k, code, node), K);
+    if (st == Game::END_TURN) G.start_turn(B.v[0]);
     G.legal(L, informed);
     u32 n = (u32)L.size() + ((G.rules.consecutive && G.corr >= 1) ? 1u : 0u);
-    u32 i = choose(n, B.v[2]);
+    u32 i = choose(n, B.v[1]);
     k += 1;
     st = G.apply(i == L.size() ? STOP : L[i]);
   }
@@ -405,8 +423,8 @@ int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
 // (LEGAL + STOP-when-allowed) or the game ends before all of F is applied.
 int playout_path(DetSpace &sp, const std::vector<u32> &F, u64 seed, u32 node, u32 s, std::vector<u32> &L) {
   const u32 code = F.back();
-  u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
-  Block D = philox(0xFFFFFFFFu, s, code, node, k0, k1);
+  const u32 K = stream_key(seed, node);
+  Block D = philox2(s, ctr1(63, code, node), K);
   u64 rho = rank64(sp.N, D.v[0], D.v[1]);
   Game G = sp.game(sp.unrank(rho));
   Game::Step st = G.apply(F[0]);
@@ -414,8 +432,9 @@ int playout_path(DetSpace &sp, const std::vector<u32> &F, u64 seed, u32 node, u3
   u32 k = 0;
   while (true) {
     if (st == Game::FINISH) return fi < F.size() ? -1 : G.winner();
-    Block B = philox(k, s, code, node, k0, k1);
-    if (st == Game::END_TURN) G.start_turn(B.v[0], B.v[1]);
+    if (k > 62) throw std::runtime_error("more than 63 decisions in one playout");
+    Block B = philox2(s, ctr1(k, code, node), K);
+    if (st == Game::END_TURN) G.start_turn(B.v[0]);
     G.legal(L);
     const bool stop_ok = G.rules.consecutive && G.corr >= 1;
     u32 n = (u32)L.size() + (stop_ok ? 1u : 0u);
@@ -425,7 +444,7 @@ int playout_path(DetSpace &sp, const std::vector<u32> &F, u64 seed, u32 node, u3
       bool ok = (a == STOP) ? stop_ok : (std::find(L.begin(), L.end(), a) != L.end());
       if (!ok) return -1;
     } else {
-      u32 i = choose(n, B.v[2]);
+      u32 i = choose(n, B.v[1]);
       a = (i == L.size()) ? STOP : L[i];
     }
     k += 1;
@@ -441,9 +460,16 @@ extern "C" {
 
 const char *oracle_last_error() { return g_err.c_str(); }
 
-void oracle_philox(const uint32_t *ctr, const uint32_t *key, uint32_t *out) {
-  Block b = philox(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]);
-  std::memcpy(out, b.v, 16);
+void oracle_philox2(const uint32_t *ctr, uint32_t key, uint32_t *out) {
+  Block b = philox2(ctr[0], ctr[1], key);
+  std::memcpy(out, b.v, 8);
+}
+
+uint32_t oracle_stream_key(uint64_t seed, uint32_t node) { return stream_key(seed, node); }
+
+void oracle_step_block(uint64_t seed, uint32_t node, uint32_t code, uint32_t s, uint32_t t, uint32_t *out) {
+  Block b = philox2(s, ctr1(t, code, node), stream_key(seed, node));
+  std::memcpy(out, b.v, 8);
 }
 
 int oracle_count(const int32_t *obs, uint64_t *N) {
