@@ -317,14 +317,13 @@ const State *as_state(const dvc_state *s) {
   return st->magic == kMagic ? st : nullptr;
 }
 
-// Batch-invariant KParams fields: Philox key + round keys, root state, plan/table.
+// Batch-invariant KParams fields: stream key K(seed, node) as Philox2x32 round
+// keys (§R3), root state, plan/table.
 void fill_kparams(KParams &kp, const State *st, uint64_t seed, uint32_t node_id, uint32_t n_actions,
                   const PlanEntry *plan, const DeviceScratch *d) {
-  kp.k0 = (uint32_t)seed; kp.k1 = (uint32_t)(seed >> 32);
-  for (int r = 0; r < 10; ++r) {
-    kp.rk[2 * r] = kp.k0 + (uint32_t)r * 0x9E3779B9u;
-    kp.rk[2 * r + 1] = kp.k1 + (uint32_t)r * 0xBB67AE85u;
-  }
+  kp.seed_lo = (uint32_t)seed; kp.seed_hi = (uint32_t)(seed >> 32);
+  const uint32_t K = stream_key(kp.seed_lo, kp.seed_hi, node_id);
+  for (int r = 0; r < 10; ++r) kp.rk[r] = K + (uint32_t)r * kPhiloxW;
   kp.node = node_id;
   kp.A = n_actions;
   kp.g0 = (uint32_t)st->viewer;

@@ -22,7 +22,7 @@
 
 namespace dvc {
 
-#ifndef DVC_REFILL_MINB
+#ifndef DVC_REFILL_MINB   // 4 (64-register cap) measured 2% slower on C2
 #define DVC_REFILL_MINB 3   // min resident 256-thread blocks per SM (register cap)
 #endif
 
@@ -81,12 +81,13 @@ __device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P,
 }
 
 // Start of playout (a, s): determinization block D, table lookup (a2), root
-// action (a3).  Returns the step state.
+// action (a3).  Returns the step state.  cb = ctr_base(code, node) (§R3).
 template <int P, bool JOK, bool CONS, int MODE>
-__device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t code, uint32_t meta,
+__device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t cb, uint32_t meta,
                                                   const KParams &kp) {
   constexpr bool PATH = MODE == kModePath;
-  const uint4 D = philox_rk(0xFFFFFFFFu, s, kp.crn ? kCrnWord : code, kp.node, kp);
+  // cb = ctr_base(code, node); under CRN the D block takes the CRN word's base
+  const uint2 D = philox_rk(s, (kp.crn ? ctr_base(kCrnWord, kp.node) : cb) | kDetStep, kp);
   determinize<P>(S, D, kp);
   uint32_t t;
   bool correct;
@@ -98,11 +99,11 @@ __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_
 
 // Decision step k of a running playout (a4), given its Philox block B_k.
 template <int P, bool JOK, bool CONS, int MODE>
-__device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint4 B, uint32_t k,
+__device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint2 B, uint32_t k,
                                                const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                const KParams &kp, uint32_t plen) {
   constexpr bool PATH = MODE == kModePath;
-  turn_start<P, JOK>(S, st == END_TURN, B.x, B.y, kp);
+  turn_start<P, JOK>(S, st == END_TURN, B.x, kp);
 #ifdef DVC_DEBUG
   dbg_check_state<P, JOK>(S, kp);
   if (!(S.H[0] & ~S.V)) dbg_fail(kp, 5);                       // the mover is alive
@@ -121,9 +122,9 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
     S.fi += 1;
     if (illegal) return VOID;
   } else if constexpr (MODE == kModeInformed) {
-    stop = decide_informed<P, JOK, CONS>(S, B.z, kp, &t, &correct);
+    stop = decide_informed<P, JOK, CONS>(S, B.y, kp, &t, &correct);
   } else {
-    stop = decide<P, JOK, CONS>(S, B.z, kp, &t, &correct);
+    stop = decide<P, JOK, CONS>(S, B.y, kp, &t, &correct);
   }
 #ifdef DVC_DEBUG
   const uint32_t r = stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
@@ -145,11 +146,10 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
-__device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t code,
+__device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t cb,
                                                  const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                  const KParams &kp) {
-  return step_block<P, JOK, CONS, MODE>(S, st, philox_rk(k, s, code, kp.node, kp), k, meta_of_a, path_of, a, kp,
-                                        kp.path_len);
+  return step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, cb | k, kp), k, meta_of_a, path_of, a, kp, kp.path_len);
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
@@ -160,11 +160,11 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kp.total; w += stride) {
     const uint32_t a = div_per(w, kp);
     const uint32_t s = kp.s0 + (w - a * kp.n_per);
-    const uint32_t code = sm.codes[a], meta = sm.meta[a];
+    const uint32_t cb = ctr_base(sm.codes[a], kp.node), meta = sm.meta[a];
     Sim<P> S;
-    uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, code, meta, kp);
+    uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, kp);
     for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
-      st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
+      st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, cb, sm.meta, sm.path, a, kp);
     record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
   flush_hist(sm.hist, kp, P);
@@ -184,14 +184,14 @@ constexpr uint32_t kRing = kRingSlots;
 
 template <int P>
 struct RingView {
-  // AoS, kRingVecs x 16 B per slot: a pop is 3-4 LDS.128 -- pops run in a
+  // AoS, kRingVecs x 16 B per slot: a pop is 3 LDS.128 -- pops run in a
   // divergent region with ~2 lanes, so instructions, not bank conflicts, are
   // what they cost.  Words: H[P], V, Q, ji, packed
-  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, code, then
-  // (DVC_PREFETCH_B) the playout's first step block B_0.
+  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, and the
+  // playout's Philox counter word c1 for step 0 (ctr_base(code, node), §R3).
   uint4 *base;
   __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
-                                      uint32_t code, uint4 B0) const {
+                                      uint32_t c1) const {
     uint32_t w[12];
 #pragma unroll
     for (int d = 0; d < P; ++d) w[d] = S.H[d];
@@ -201,21 +201,19 @@ struct RingView {
     w[P + 3] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (S.fi << 28);
     w[P + 4] = a;
     w[P + 5] = s;
-    w[P + 6] = code;
+    w[P + 6] = c1;
 #pragma unroll
     for (int j = P + 7; j < 12; ++j) w[j] = 0;
     uint4 *b = base + kRingVecs * i;
     b[0] = make_uint4(w[0], w[1], w[2], w[3]);
     b[1] = make_uint4(w[4], w[5], w[6], w[7]);
     if (P + 7 > 8) b[2] = make_uint4(w[8], w[9], w[10], w[11]);
-    if (kRingVecs == 4) b[3] = B0;
   }
   __device__ __forceinline__ void get(uint32_t i, Sim<P> &S, uint32_t &st, uint32_t &a, uint32_t &s,
-                                      uint32_t &code, uint4 &B0) const {
+                                      uint32_t &c1) const {
     const uint4 *b = base + kRingVecs * i;
     const uint4 q0 = b[0], q1 = b[1];
     const uint4 q2 = (P + 7 > 8) ? b[2] : make_uint4(0, 0, 0, 0);
-    if (kRingVecs == 4) B0 = b[3];
     const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
 #pragma unroll
     for (int d = 0; d < P; ++d) S.H[d] = w[d];
@@ -230,7 +228,7 @@ struct RingView {
     S.fi = pk >> 28;
     a = w[P + 4];
     s = w[P + 5];
-    code = w[P + 6];
+    c1 = w[P + 6];
   }
 };
 
@@ -251,21 +249,22 @@ __global__ void __launch_bounds__(256, DVC_REFILL_MINB) rollout_refill_kernel(co
   // slices of ONE action, so no per-lane division).  The next batch index is
   // claimed one batch ahead (lane 0's atomicAdd result is only read at the
   // next produce), so the atomic's latency is hidden.
-  uint32_t ca = 0, cs = 0, ce = 0, ccode = 0, cmeta = 0;
+  uint32_t ca = 0, cs = 0, ce = 0, ccb = 0, cmeta = 0;   // ccb = ctr_base(code of ca, node)
   bool drained = false;
   const uint32_t n_batches = kp.A * kp.nb;
   uint32_t pref = 0;
   if (lane == 0) pref = atomicAdd(kp.counter, 1u);
   uint32_t head = 0, count = 0;       // ring (warp-uniform)
   bool active = false;
-  uint32_t a = 0, s = 0, code = 0, st = FINISH, k = 0;
-  uint4 B = make_uint4(0, 0, 0, 0);   // DVC_PREFETCH_B: the running playout's block for step k
+  // the running playout: action, sim, step state and its Philox counter word
+  // c1 = ctr_base(code, node) | k, advanced by one per decision step (§R3)
+  uint32_t a = 0, s = 0, st = FINISH, c1 = 0;
   Sim<P> S;
   while (true) {
     // ---- produce: the whole warp starts up to 32 playouts
     while (count < 32u && !(drained && cs >= ce)) {
       uint32_t rem = ce - cs;
-      uint32_t na = 0, ns = 0, ne = 0, ncode = 0, nmeta = 0;
+      uint32_t na = 0, ns = 0, ne = 0, ncb = 0, nmeta = 0;
       bool got = false;
       if (rem < 32u && !drained) {
         const uint32_t b = __shfl_sync(0xFFFFFFFFu, pref, 0);
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(256, DVC_REFILL_MINB) rollout_refill_kernel(co
           na = b / kp.nb;
           ns = (b - na * kp.nb) * kBatch;       // relative to s0 (no u32 overflow at 2^32)
           ne = min(ns + kBatch, kp.n_per);
-          ncode = sm.codes[na];
+          ncb = ctr_base(sm.codes[na], kp.node);
           nmeta = sm.meta[na];
           got = true;
         } else {
@@ -282,44 +281,37 @@ __global__ void __launch_bounds__(256, DVC_REFILL_MINB) rollout_refill_kernel(co
         }
       }
       bool valid = false;
-      uint32_t pa = 0, ps = 0, pcode = 0, pmeta = 0;
+      uint32_t pa = 0, ps = 0, pcb = 0, pmeta = 0;
       if (lane < rem) {
-        pa = ca; ps = kp.s0 + cs + lane; pcode = ccode; pmeta = cmeta; valid = true;
+        pa = ca; ps = kp.s0 + cs + lane; pcb = ccb; pmeta = cmeta; valid = true;
       } else if (got && ns + (lane - rem) < ne) {
-        pa = na; ps = kp.s0 + ns + (lane - rem); pcode = ncode; pmeta = nmeta; valid = true;
+        pa = na; ps = kp.s0 + ns + (lane - rem); pcb = ncb; pmeta = nmeta; valid = true;
       }
       if (got) {
-        ca = na; ccode = ncode; cmeta = nmeta; ce = ne;
+        ca = na; ccb = ncb; cmeta = nmeta; ce = ne;
         cs = min(ns + (32u - rem), ne);
       } else {
         cs = min(cs + 32u, ce);
       }
       Sim<P> T;
       uint32_t pst = FINISH;
-      uint4 B0 = make_uint4(0, 0, 0, 0);
       if (valid) {
-        if (DVC_PREFETCH_B) B0 = philox_rk(0u, ps, pcode, kp.node, kp);
-        pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcode, pmeta, kp);
+        pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcb, pmeta, kp);
         if (pst == FINISH) {                    // decided by the root action alone
           record<MODE>(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
           valid = false;
         }
       }
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, valid);
-      if (valid) ring.put((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcode, B0);
+      if (valid) ring.put((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcb);
       count += __popc(m);
       __syncwarp();
     }
     // ---- one decision step for every running lane
     if (active) {
-      if (DVC_PREFETCH_B) {
-        const uint4 Bn = philox_rk(k + 1u, s, code, kp.node, kp);   // next step's block, independent chain
-        st = step_block<P, JOK, CONS, MODE>(S, st, B, k, sm.meta, sm.path, a, kp, kp.path_len);
-        B = Bn;
-      } else {
-        st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, code, sm.meta, sm.path, a, kp);
-      }
-      ++k;
+      st = step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+                                          kp.path_len);
+      ++c1;
       if (st == FINISH || st == VOID) {
         record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
         active = false;
@@ -332,8 +324,7 @@ __global__ void __launch_bounds__(256, DVC_REFILL_MINB) rollout_refill_kernel(co
       if (take) {
         const uint32_t rank = __popc(need & lt_mask);
         if (!active && rank < take) {
-          ring.get((head + rank) & (kRing - 1u), S, st, a, s, code, B);
-          k = 0;
+          ring.get((head + rank) & (kRing - 1u), S, st, a, s, c1);
           active = true;
         }
         head = (head + take) & (kRing - 1u);
@@ -431,7 +422,7 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
     }
     __syncthreads();
     const uint32_t best = s_best;
-    const uint32_t code = kp.codes[best], meta = kp.meta[best];
+    const uint32_t cb = ctr_base(kp.codes[best], kp.node), meta = kp.meta[best];
     const uint32_t sbase = (uint32_t)vis[best];
     // ---- simulation: sims [visits, visits + n) of the chosen child
     uint32_t cnt = 0;
@@ -439,12 +430,12 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
       const uint32_t s = sbase + i;
       Sim<P> S;
       constexpr int MODE = INF ? kModeInformed : kModePlain;
-      uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, code, meta, kp);
+      uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, kp);
       // latency-bound loop: B_{k+1} is independent of the state, so it is
       // generated while step k runs
-      uint4 B = philox_rk(0u, s, code, kp.node, kp);
+      uint2 B = philox_rk(s, cb, kp);
       for (uint32_t k = 0; st != FINISH; ++k) {
-        const uint4 Bn = philox_rk(k + 1u, s, code, kp.node, kp);
+        const uint2 Bn = philox_rk(s, cb | (k + 1u), kp);
         st = step_block<P, JOK, CONS, MODE>(S, st, B, k, nullptr, nullptr, 0, kp, 0u);
         B = Bn;
       }
@@ -735,6 +726,7 @@ __global__ void __launch_bounds__(128) deep_search_kernel(const __grid_constant_
     // ---- the batch: nb actions x n sims, F = path + [action]
     const uint32_t nb = __ldcg(&B->nb), plen = __ldcg(&B->plen), list = __ldcg(&B->list);
     const uint32_t node = __ldcg(&B->node_word), s0 = __ldcg(&B->s0);
+    const uint32_t K = stream_key(kp.seed_lo, kp.seed_hi, node);   // the batch node's stream key (§R3)
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) { swin[i] = 0; svoid[i] = 0; }
     if (threadIdx.x < kMaxPath) s_path[threadIdx.x] = __ldcg(&B->path_meta[threadIdx.x]);
     __syncthreads();
@@ -746,8 +738,8 @@ __global__ void __launch_bounds__(128) deep_search_kernel(const __grid_constant_
       const uint32_t a = w / da.n, s = s0 + (w - a * da.n);
       const uint32_t code = list == 2u ? lcode : codes[a], meta = list == 2u ? lmeta : metas[a];
       Sim<P> S;
-      const uint4 D = philox_rk(0xFFFFFFFFu, s, code, node, kp);
-      determinize<P>(S, D, kp);
+      const uint32_t cb = ctr_base(code, node);
+      determinize<P>(S, philox2x32_10(s, cb | kDetStep, K), kp);
       uint32_t t;
       bool correct;
       const bool stop = root_action<P, JOK>(S, plen ? s_path[0] : meta, kp, &t, &correct);
@@ -755,7 +747,7 @@ __global__ void __launch_bounds__(128) deep_search_kernel(const __grid_constant_
       uint32_t st = stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
       const uint32_t meta_a[1] = {meta};
       for (uint32_t k = 0; st != FINISH && st != VOID; ++k) {
-        st = step_block<P, JOK, CONS, kModePath>(S, st, philox_rk(k, s, code, node, kp), k, meta_a, s_path, 0u,
+        st = step_block<P, JOK, CONS, kModePath>(S, st, philox2x32_10(s, cb | k, K), k, meta_a, s_path, 0u,
                                                   kp, plen);
         if (k > 4096u) { atomicCAS(da.status, 0, kWatchdogPlayout); st = VOID; }   // never expected
       }

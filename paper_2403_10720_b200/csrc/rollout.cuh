@@ -16,25 +16,19 @@ namespace dvc {
 
 constexpr int kMaxActions = 768;
 
-// Refill kernel (kernels.cu): the Philox block of a playout's NEXT decision
-// step is generated during the current one (an independent dependency chain
-// for the scheduler to interleave with the step's serial game logic), so a
-// started playout carries its first step block B_0 in its ring slot.
-#ifndef DVC_PREFETCH_B
-#define DVC_PREFETCH_B 0   // measured: -7% on C2, -3% on C4 (more Philox work, bigger ring slots)
-#endif
 constexpr uint32_t kRingSlots = 64;                          // started playouts per warp
-constexpr uint32_t kRingVecs = DVC_PREFETCH_B ? 4u : 3u;     // 16 B vectors per ring slot
+constexpr uint32_t kRingVecs = 3u;                           // 16 B vectors per ring slot
 
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
-constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's counter word z under common random numbers (no action code)
+constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's code under common random numbers (no action code, §R3)
+constexpr uint32_t kDetStep = 63u;           // step field of the determinization block D (§R3)
 // Kernel modes: root batches, deep-tree (forced path) batches, informed policy
 // (§R10), root batches writing the per-playout winner trace (parity tests).
 constexpr int kModePlain = 0, kModePath = 1, kModeInformed = 2, kModeTrace = 3;
 
 struct KParams {
-  uint32_t k0, k1;        // Philox key = (lo32(seed), hi32(seed))
-  uint32_t node;          // Philox counter word w
+  uint32_t seed_lo, seed_hi;  // the batch seed (device searches derive per-batch stream keys from it)
+  uint32_t node;          // tree node id of the batch (stream key and counter bits, §R3)
   uint32_t s0;            // first sim index of this launch
   uint32_t n_per;         // sims per action in this launch
   uint32_t total;         // A * n_per (<= 2^31)
@@ -53,7 +47,7 @@ struct KParams {
   uint64_t div_magic;     // ceil(2^64 / n_per) (0 when n_per == 1): item / n_per = umul64hi(item, magic)
   uint32_t nb;            // refill kernel: kBatch-sized sim batches per action = ceil(n_per / kBatch)
   uint32_t crn;           // 1: determinization block keyed by kCrnWord, not the action code (§R3 CRN)
-  uint32_t rk[20];        // Philox round keys (k0 + r*W0, k1 + r*W1), r = 0..9: read from the
+  uint32_t rk[10];        // Philox2x32 round keys K(seed, node) + r*W, r = 0..9: read from the
                           // constant bank as instruction operands (no registers, no adds)
   const uint4 *table;     // N entries (H1, H2, H3, jinfo) or null -> inline unrank
   const uint8_t *plan;    // DetPlanHdr image (inline unrank / table build)
@@ -108,29 +102,45 @@ struct DeepArgs {
 };
 
 // ----------------------------------------------------------------- RNG (§R3)
-__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                               uint32_t k0, uint32_t k1) {
+// Philox2x32-10: one round (hi, lo) = M * c0; (c0, c1) <- (hi ^ k ^ c1, lo);
+// the key is bumped by W between rounds.
+constexpr uint32_t kPhiloxM = 0xD256D193u, kPhiloxW = 0x9E3779B9u;
+
+__host__ __device__ __forceinline__ uint2 philox2x32_10(uint32_t c0, uint32_t c1, uint32_t k) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    const uint64_t p = (uint64_t)kPhiloxM * c0;
+    const uint32_t hi = (uint32_t)(p >> 32), lo = (uint32_t)p;
+    c0 = hi ^ k ^ c1;
+    c1 = lo;
+    k += kPhiloxW;
   }
-  return make_uint4(c0, c1, c2, c3);
+  return make_uint2(c0, c1);
 }
 
-// Same function with the batch's precomputed round keys.
-__device__ __forceinline__ uint4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const KParams &kp) {
+// Stream key K(seed, node) = word 0 of Philox2x32-10((lo32 seed, hi32 seed), node).
+__host__ __device__ __forceinline__ uint32_t stream_key(uint32_t seed_lo, uint32_t seed_hi, uint32_t node) {
+  return philox2x32_10(seed_lo, seed_hi, node).x;
+}
+
+// Counter word c1 without the step field: code12(code) << 6 | (node mod 2^14) << 18.
+__host__ __device__ __forceinline__ uint32_t ctr_base(uint32_t code, uint32_t node) {
+  const uint32_t c12 = code == 0xFFFFFFFFu ? 0xFFFu
+                     : code == kCrnWord    ? 0xFFEu
+                     : ((code >> 24) << 10) | (((code >> 16) & 0xFFu) << 5) | (code & 0xFFFFu);
+  return (c12 << 6) | ((node & 0x3FFFu) << 18);
+}
+
+// The batch's block for counter (s, c1), with the precomputed round keys.
+__device__ __forceinline__ uint2 philox_rk(uint32_t s, uint32_t c1, const KParams &kp) {
+  uint32_t c0 = s;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ kp.rk[2 * r], n2 = hi0 ^ c3 ^ kp.rk[2 * r + 1];
-    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    const uint32_t hi = __umulhi(kPhiloxM, c0), lo = kPhiloxM * c0;
+    c0 = hi ^ kp.rk[r] ^ c1;
+    c1 = lo;
   }
-  return make_uint4(c0, c1, c2, c3);
+  return make_uint2(c0, c1);
 }
 
 __device__ __forceinline__ uint32_t choose(uint32_t n, uint32_t w) { return __umulhi(w, n); }
@@ -291,11 +301,12 @@ __device__ __forceinline__ uint32_t line_pos(uint32_t Hp, uint32_t v, uint32_t j
 
 // Turn start (DESIGN.md §R5 END_TURN): the next alive player after g becomes
 // the mover (relative seats rotate), pend/corr reset, and it draws the
-// (choose(|Q|, wx))-th smallest pool key (joker gap from wy).  Written
+// (choose(|Q|, w))-th smallest pool key (a drawn joker's gap from the
+// remainder (w * |Q|) mod 2^32, §R3).  Written
 // branch-free under the predicate `et` so lanes at different phases of a turn
 // do not diverge; the joker insertion is the only (rare) real branch.
 template <int P, bool JOK>
-__device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t wx, uint32_t wy, const KParams &kp) {
+__device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const KParams &kp) {
   if (P == 2) {
     const uint32_t h0 = et ? S.H[1] : S.H[0], h1 = et ? S.H[0] : S.H[1];
     S.H[0] = h0; S.H[1] = h1;
@@ -319,7 +330,8 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t wx, uint
     S.g += delta;
     S.g = S.g >= (uint32_t)P ? S.g - P : S.g;
   }
-  const uint32_t t = nth_bit(S.Q, choose((uint32_t)__popc(S.Q), wx));
+  const uint64_t wq = (uint64_t)w * (uint32_t)__popc(S.Q);   // (choose, remainder) in one IMAD.WIDE
+  const uint32_t t = nth_bit(S.Q, (uint32_t)(wq >> 32));
   const bool dr = et && S.Q != 0;
   const uint32_t H0 = S.H[0];
   if (JOK) {
@@ -328,7 +340,7 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t wx, uint
     const uint32_t Hn = H0 & kp.numm;
     if (dr && t >= kp.JB) {
       // drawn joker: uniform gap in [0, len]; relative order with the other joker
-      const uint32_t gam = choose((uint32_t)__popc(H0) + 1u, wy);
+      const uint32_t gam = choose((uint32_t)__popc(H0) + 1u, (uint32_t)wq);
       const uint32_t is_w = t - kp.JB;
       const bool has_other = is_w ? hasB : hasW;
       uint32_t sj = gam;                          // numbered tiles left of the new joker
@@ -435,12 +447,12 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
 }
 
 // One random decision (DESIGN.md §R5 loop body after the draw): i =
-// choose(n, wz) over LEGAL(g) (+ STOP last).  Returns true for STOP; else the
+// choose(n, w) over LEGAL(g) (+ STOP last), w = b1.  Returns true for STOP; else the
 // targeted hidden tile t and whether the guessed value equals it.  The value
 // itself is never materialised: the vidx-th available value of t's colour
 // equals t exactly when vidx = #available values of that colour below t.
 template <int P, bool JOK, bool CONS>
-__device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t wz, const KParams &kp, uint32_t *t_out,
+__device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t w, const KParams &kp, uint32_t *t_out,
                                        bool *correct) {
   const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
   const uint32_t aB = avail & kEven, aW = avail & kOdd;
@@ -454,7 +466,7 @@ __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t wz, const KPara
     tot += cnt[d];
   }
   const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
-  uint32_t x = choose(n, wz);
+  uint32_t x = choose(n, w);
   const bool stop = CONS && x >= tot;
   uint32_t d = 1;
   if (P > 2) {
@@ -571,7 +583,7 @@ __device__ __forceinline__ void informed_select(const InfCtx &c, uint32_t Hd, ui
 
 // One informed decision: as decide(), over the order-aware list.
 template <int P, bool JOK, bool CONS>
-__device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t wz, const KParams &kp, uint32_t *t_out,
+__device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t w, const KParams &kp, uint32_t *t_out,
                                                 bool *correct) {
   const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
   InfCtx c;
@@ -587,7 +599,7 @@ __device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t wz, co
     tot += cnt[d];
   }
   const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
-  uint32_t x = choose(n, wz);
+  uint32_t x = choose(n, w);
   const bool stop = CONS && x >= tot;
   uint32_t d = 1;
   if (P > 2) {
@@ -679,7 +691,7 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
 
 // Determinization (a2): state of playout with determinization block D.
 template <int P>
-__device__ __forceinline__ void determinize(Sim<P> &S, uint4 D, const KParams &kp) {
+__device__ __forceinline__ void determinize(Sim<P> &S, uint2 D, const KParams &kp) {
   const uint64_t rho = rank64(kp.N, D.x, D.y);
   const uint4 e = kp.table ? __ldg(kp.table + rho) : unrank(kp.plan, rho);
   S.H[0] = kp.Hv;
