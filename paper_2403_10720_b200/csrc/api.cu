@@ -404,9 +404,9 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
                                   : kModePlain;
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
   size_t smem = ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
-  if (variant == 0)   // + the per-warp rings: kRingSlots x kRingVecs x 16 B, 16 B aligned (kernels.cu RingView)
+  if (variant == 0)   // + the per-warp rings: kRingSlots x ring_vecs(P) x 16 B, 16 B aligned (kernels.cu RingView)
     smem = (((size_t)n_actions * (P + 3) + kMaxPath + 3) & ~(size_t)3) * sizeof(uint32_t) +
-           (size_t)(block / 32) * kRingSlots * kRingVecs * 16;
+           (size_t)(block / 32) * kRingSlots * ring_vecs(P) * 16;
   if (variant == 0 && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
   const int grid_opt = (int)g_grid.load();
   int grid_full = grid_opt;

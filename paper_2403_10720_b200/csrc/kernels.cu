@@ -22,8 +22,15 @@
 
 namespace dvc {
 
-#ifndef DVC_REFILL_MINB   // 4 (64-register cap) measured 2% slower on C2
-#define DVC_REFILL_MINB 3   // min resident 256-thread blocks per SM (register cap)
+// Register cap of the refill kernel as min resident 256-thread blocks per SM.
+// Two players without jokers: 4 (64 registers; 8 blocks of 128 per SM), +1.3%
+// on C2; with jokers or more players the cap costs more than the occupancy
+// gains (C3 -3%, C4 -2.4%), so 3.
+#ifndef DVC_REFILL_MINB2
+#define DVC_REFILL_MINB2 4
+#endif
+#ifndef DVC_REFILL_MINB
+#define DVC_REFILL_MINB 3
 #endif
 
 constexpr uint32_t kBatch = 32;   // sims per work batch of the refill kernel (one produce round)
@@ -184,15 +191,16 @@ constexpr uint32_t kRing = kRingSlots;
 
 template <int P>
 struct RingView {
-  // AoS, kRingVecs x 16 B per slot: a pop is 3 LDS.128 -- pops run in a
+  // AoS, ring_vecs(P) x 16 B per slot: a pop is 3-4 LDS.128 -- pops run in a
   // divergent region with ~2 lanes, so instructions, not bank conflicts, are
   // what they cost.  Words: H[P], V, Q, ji, packed
-  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, and the
-  // playout's Philox counter word c1 for step 0 (ctr_base(code, node), §R3).
+  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, the playout's
+  // Philox counter word c1 for step 0 (ctr_base(code, node), §R3).
+  static constexpr uint32_t V = ring_vecs(P);
   uint4 *base;
   __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
                                       uint32_t c1) const {
-    uint32_t w[12];
+    uint32_t w[16];
 #pragma unroll
     for (int d = 0; d < P; ++d) w[d] = S.H[d];
     w[P + 0] = S.V;
@@ -203,18 +211,20 @@ struct RingView {
     w[P + 5] = s;
     w[P + 6] = c1;
 #pragma unroll
-    for (int j = P + 7; j < 12; ++j) w[j] = 0;
-    uint4 *b = base + kRingVecs * i;
-    b[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    b[1] = make_uint4(w[4], w[5], w[6], w[7]);
-    if (P + 7 > 8) b[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    for (int j = P + 7; j < 16; ++j) w[j] = 0;
+    uint4 *b = base + V * i;
+#pragma unroll
+    for (uint32_t q = 0; q < V; ++q) b[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
   __device__ __forceinline__ void get(uint32_t i, Sim<P> &S, uint32_t &st, uint32_t &a, uint32_t &s,
                                       uint32_t &c1) const {
-    const uint4 *b = base + kRingVecs * i;
-    const uint4 q0 = b[0], q1 = b[1];
-    const uint4 q2 = (P + 7 > 8) ? b[2] : make_uint4(0, 0, 0, 0);
-    const uint32_t w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+    const uint4 *b = base + V * i;
+    uint32_t w[16];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      const uint4 v = q < V ? b[q] : make_uint4(0, 0, 0, 0);
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
 #pragma unroll
     for (int d = 0; d < P; ++d) S.H[d] = w[d];
     S.V = w[P + 0];
@@ -238,13 +248,14 @@ __host__ __device__ __forceinline__ uint32_t ring_word_offset(uint32_t A, int P)
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
-__global__ void __launch_bounds__(256, DVC_REFILL_MINB) rollout_refill_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC_REFILL_MINB)
+    rollout_refill_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
   const Smem sm = setup_smem(kp, P);
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * kRingVecs * kRing};
+  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * ring_vecs(P) * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
   // slices of ONE action, so no per-lane division).  The next batch index is
   // claimed one batch ahead (lane 0's atomicAdd result is only read at the
