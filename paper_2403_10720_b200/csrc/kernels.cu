@@ -25,7 +25,8 @@ namespace dvc {
 // Register cap of the refill kernel as min resident 256-thread blocks per SM.
 // Two players without jokers: 4 (64 registers; 8 blocks of 128 per SM), +1.3%
 // on C2; with jokers or more players the cap costs more than the occupancy
-// gains (C3 -3%, C4 -2.4%), so 3.
+// gains (C3 -3%, C4 -2.4%), so 3.  Tighter caps for two players (56 or 52
+// registers, 9-10 blocks) measured -3% / -4%.
 #ifndef DVC_REFILL_MINB2
 #define DVC_REFILL_MINB2 4
 #endif
@@ -193,11 +194,16 @@ template <int P>
 struct RingView {
   // AoS, ring_vecs(P) x 16 B per slot: a pop is 3-4 LDS.128 -- pops run in a
   // divergent region with ~2 lanes, so instructions, not bank conflicts, are
-  // what they cost.  Words: H[P], V, Q, ji, packed
-  // (g | pend << 8 | corr << 16 | st << 24 | fi << 28), a, s, the playout's
-  // Philox counter word c1 for step 0 (ctr_base(code, node), §R3).
-  static constexpr uint32_t V = ring_vecs(P);
+  // what they cost.  Words: H[P], V, Q, ji, then for two players (12 words,
+  // 3 vectors) g, pend, corr, st | fi << 4 unpacked -- no shifts and masks on
+  // a pop -- and for more players the packed (g | pend << 8 | corr << 16 |
+  // st << 24 | fi << 28); then a, s and the playout's Philox counter word c1
+  // for step 0 (ctr_base(code, node), §R3).
+  static constexpr bool kUnpacked = P == 2;
+  static constexpr int kNW = kUnpacked ? P + 10 : P + 7;   // words used
+  static constexpr uint32_t V = (kNW + 3) / 4;
   uint4 *base;
+  template <bool PATH>
   __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
                                       uint32_t c1) const {
     uint32_t w[16];
@@ -206,16 +212,25 @@ struct RingView {
     w[P + 0] = S.V;
     w[P + 1] = S.Q;
     w[P + 2] = S.ji;
-    w[P + 3] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (S.fi << 28);
-    w[P + 4] = a;
-    w[P + 5] = s;
-    w[P + 6] = c1;
+    int j = P + 3;
+    if (kUnpacked) {
+      w[j++] = S.g;
+      w[j++] = S.pend;
+      w[j++] = S.corr;
+      w[j++] = PATH ? (st | (S.fi << 4)) : st;   // fi exists in deep-tree batches only
+    } else {
+      w[j++] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (PATH ? S.fi << 28 : 0u);
+    }
+    w[j++] = a;
+    w[j++] = s;
+    w[j++] = c1;
 #pragma unroll
-    for (int j = P + 7; j < 16; ++j) w[j] = 0;
+    for (int q = kNW; q < 16; ++q) w[q] = 0;
     uint4 *b = base + V * i;
 #pragma unroll
     for (uint32_t q = 0; q < V; ++q) b[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
+  template <bool PATH>
   __device__ __forceinline__ void get(uint32_t i, Sim<P> &S, uint32_t &st, uint32_t &a, uint32_t &s,
                                       uint32_t &c1) const {
     const uint4 *b = base + V * i;
@@ -230,15 +245,25 @@ struct RingView {
     S.V = w[P + 0];
     S.Q = w[P + 1];
     S.ji = w[P + 2];
-    const uint32_t pk = w[P + 3];
-    S.g = pk & 0xFFu;
-    S.pend = (pk >> 8) & 0xFFu;
-    S.corr = (pk >> 16) & 0xFFu;
-    st = (pk >> 24) & 0xFu;
-    S.fi = pk >> 28;
-    a = w[P + 4];
-    s = w[P + 5];
-    c1 = w[P + 6];
+    int j = P + 3;
+    if (kUnpacked) {
+      S.g = w[j++];
+      S.pend = w[j++];
+      S.corr = w[j++];
+      const uint32_t sf = w[j++];
+      st = PATH ? (sf & 0xFu) : sf;          // fi is nonzero in deep-tree batches only
+      S.fi = PATH ? (sf >> 4) : 0u;
+    } else {
+      const uint32_t pk = w[j++];
+      S.g = pk & 0xFFu;
+      S.pend = (pk >> 8) & 0xFFu;
+      S.corr = (pk >> 16) & 0xFFu;
+      st = (pk >> 24) & 0xFu;
+      S.fi = PATH ? pk >> 28 : 0u;
+    }
+    a = w[j++];
+    s = w[j++];
+    c1 = w[j++];
   }
 };
 
@@ -255,7 +280,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * ring_vecs(P) * kRing};
+  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * RingView<P>::V * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
   // slices of ONE action, so no per-lane division).  The next batch index is
   // claimed one batch ahead (lane 0's atomicAdd result is only read at the
@@ -314,7 +339,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
         }
       }
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, valid);
-      if (valid) ring.put((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcb);
+      if (valid) ring.template put<PATH>((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcb);
       count += __popc(m);
       __syncwarp();
     }
@@ -335,7 +360,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
       if (take) {
         const uint32_t rank = __popc(need & lt_mask);
         if (!active && rank < take) {
-          ring.get((head + rank) & (kRing - 1u), S, st, a, s, c1);
+          ring.template get<PATH>((head + rank) & (kRing - 1u), S, st, a, s, c1);
           active = true;
         }
         head = (head + take) & (kRing - 1u);
