@@ -96,9 +96,13 @@ def observe(game, viewer):
             "correct_this_turn": game.corr, "truth": truth}
 
 
-def make_position(rules, per, deal_seed, turns, extra_correct=0, until_pool_empty=False):
+def make_position(rules, per, deal_seed, turns, extra_correct=0, until_pool_empty=False, max_attempts=None):
+    """max_attempts: give up (return None) after that many redraws (tests'
+    random positions; the committed fixtures use the unbounded default)."""
     attempt = 0
     while True:
+        if max_attempts is not None and attempt >= max_attempts:
+            return None
         rng = random.Random(deal_seed * 1000003 + attempt)
         attempt += 1
         game = _deal(rules, per, rng)
