@@ -195,6 +195,15 @@ __device__ __forceinline__ void probe_w(uint32_t &nk, uint32_t &base, uint32_t h
       : "+r"(nk), "+r"(base) : "r"(hB), "r"(hW), "r"(nB), "r"(nW), "r"(x), "n"(32 - B), "n"(B));
 }
 
+// c ? a : b for c in {0, 1}, as b + c * (a - b) in two IMADs (FMA pipe)
+// instead of a SEL (ALU pipe); PTX so the compiler keeps the form.
+__device__ __forceinline__ uint32_t blend01(uint32_t c, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .u32 t;\n\tmad.lo.u32 t, %3, -1, %2;\n\tmad.lo.u32 %0, %1, t, %3;\n\t}"
+      : "=r"(r) : "r"(c), "r"(a), "r"(b));
+  return r;
+}
+
 // 0-based n-th set bit of m (must exist): fixed 5-step search, no divergence.
 __device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t n) {
   uint32_t nk = 0;
@@ -322,13 +331,14 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
     for (int d = P - 2; d >= 1; --d) delta = (S.H[d] & ~S.V) ? (uint32_t)d : delta;
     delta = et ? delta : 0u;
     // rotate the hands by delta (< 4) as a rotation by 1 if bit 0, then by 2
-    // if bit 1: 2P selects instead of P(P-1)
+    // if bit 1: 2P blends instead of P(P-1) selects, each blend two IMADs
+    // (FMA pipe) instead of a SEL (ALU pipe, the binding unit for P > 2)
 #pragma unroll
     for (int sh = 1; sh <= 2; sh <<= 1) {
-      const bool c = (delta & (uint32_t)sh) != 0u;
+      const uint32_t c = sh == 1 ? (delta & 1u) : (delta >> 1);
       uint32_t Hn[P];
 #pragma unroll
-      for (int i = 0; i < P; ++i) Hn[i] = c ? S.H[(i + sh) % P] : S.H[i];
+      for (int i = 0; i < P; ++i) Hn[i] = blend01(c, S.H[(i + sh) % P], S.H[i]);
 #pragma unroll
       for (int i = 0; i < P; ++i) S.H[i] = Hn[i];
     }
@@ -415,8 +425,8 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
   uint32_t sel = kNoKey, vidx_j = 0;
   if (JOK) {
     // hidden jokers of this line are placed first, by their thresholds.  Done
-    // branch-free for every lane (in 4-player games nearly every warp-step has
-    // some lane whose target line holds a hidden joker).
+    // branch-free for every lane (a warp-uniform skip when no lane's target
+    // holds a hidden joker measured -4.5% on C4 and -7% on C3).
     const uint32_t hb = hid & kp.numm & kEven, hw = hid & kp.numm & kOdd;
     const uint32_t kb = kap_b(ji), kw = kap_w(ji);
     const bool hidB = (hid >> kp.JB) & 1u, hidW = (hid >> (kp.JB + 1)) & 1u;
