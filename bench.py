@@ -315,8 +315,7 @@ def run_product(args):
     A, P = len(codes), st.players
     n = args.sims
     s0, s1 = rank * n, (rank + 1) * n
-    if args.kernel == "naive":
-        dvc.set_option("kernel", 1)
+    dvc.set_option("kernel", 1 if args.kernel == "naive" else 0)
     dvc.set_option("plan_cache", 0)       # plan upload + det table rebuilt inside every step
     stream = torch.cuda.current_stream()
     hist = torch.zeros((A, P), dtype=torch.int64, device=dev)

@@ -173,8 +173,11 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
                             uint64_t *d_hist, uint8_t *d_winners, int32_t device, void *cuda_stream);
 
 /* Launch options (process-wide; they never change results):
- *  "kernel"      0 = persistent warp-refill kernel (default), 1 = naive
- *                thread-per-playout kernel (the paper-style comparison)
+ *  "kernel"      0 = persistent warp-refill kernel, 1 = naive
+ *                thread-per-playout kernel (the paper-style comparison),
+ *                2 = auto (default): naive when all of a call's playouts fit in one
+ *                resident wave of naive threads (latency-bound small batches: C1
+ *                decisions, search batches), refill otherwise
  *  "block"       threads per block (1..1024 for the naive kernel; a multiple of
  *                32 up to 256 for the refill kernel; default 128)
  *  "grid"        blocks (0 = auto: resident blocks per SM x #SM, or fewer when

@@ -37,7 +37,7 @@ cudaError_t launch_flat_search(const KParams &kp, const SearchArgs &sa, int P, b
 namespace {
 
 thread_local std::string g_err;
-std::atomic<int64_t> g_kernel{0}, g_block{128}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1},
+std::atomic<int64_t> g_kernel{2}, g_block{128}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1},
     g_chunk{1ll << 31}, g_search_device{0};
 std::atomic<uint64_t> g_launches{0};
 
@@ -396,35 +396,51 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   kp.trace_stride = (uint32_t)(sim_end - sim_begin);
   kp.trace_s0 = (uint32_t)sim_begin;
 
-  const int variant = (int)g_kernel.load();
+  int variant = (int)g_kernel.load();
   const int block = (int)g_block.load();
   const int mode = kp.path_len > 0 ? kModePath
                  : path.informed  ? kModeInformed
                  : d_winners      ? kModeTrace
                                   : kModePlain;
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
-  size_t smem = ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
-  if (variant == 0)   // + the per-warp rings: kRingSlots x ring_vecs(P) x 16 B, 16 B aligned (kernels.cu RingView)
-    smem = (((size_t)n_actions * (P + 3) + kMaxPath + 3) & ~(size_t)3) * sizeof(uint32_t) +
+  auto smem_of = [&](int v) {
+    if (v != 0) return ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
+    // + the per-warp rings: kRingSlots x ring_vecs(P) x 16 B, 16 B aligned (kernels.cu RingView)
+    return (((size_t)n_actions * (P + 3) + kMaxPath + 3) & ~(size_t)3) * sizeof(uint32_t) +
            (size_t)(block / 32) * kRingSlots * ring_vecs(P) * 16;
+  };
+  // resident blocks per SM, cached per (kernel instance, block, smem)
+  auto per_sm_of = [&](int v, size_t sm, int *out) -> int {
+    const uint64_t okey = ((uint64_t)v << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
+                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)mode << 51) |
+                          ((uint64_t)block << 32) | (uint64_t)sm;
+    auto it = d->occupancy.find(okey);
+    if (it != d->occupancy.end()) { *out = it->second; return DVC_OK; }
+    cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, v, mode, block, sm, out);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    d->occupancy[okey] = *out;
+    return DVC_OK;
+  };
+  if (variant == 2) {
+    // auto: a call whose playouts all fit in one resident wave of naive
+    // threads is latency-bound -- one playout per thread finishes with the
+    // longest playout, where refill warps that claim a second batch finish
+    // later (C1: 33 us vs 51 us device span) -- anything larger takes the
+    // refill kernel's throughput
+    int ps = 0;
+    rc = per_sm_of(1, smem_of(1), &ps);
+    if (rc) return rc;
+    const uint64_t total = (uint64_t)n_actions * (sim_end - sim_begin);
+    variant = total <= (uint64_t)ps * (uint64_t)d->num_sms * (uint64_t)block ? 1 : 0;
+  }
+  const size_t smem = smem_of(variant);
   if (variant == 0 && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
   const int grid_opt = (int)g_grid.load();
   int grid_full = grid_opt;
   if (grid_opt <= 0) {
-    // resident blocks per SM, cached per (kernel instance, block, smem)
-    const uint64_t okey = ((uint64_t)variant << 60) | ((uint64_t)P << 56) | ((uint64_t)(st->jokers != 0) << 55) |
-                          ((uint64_t)(st->consecutive != 0) << 54) | ((uint64_t)mode << 51) |
-                          ((uint64_t)block << 32) | (uint64_t)smem;
     int per_sm = 0;
-    auto it = d->occupancy.find(okey);
-    if (it != d->occupancy.end()) {
-      per_sm = it->second;
-    } else {
-      cudaError_t e = kernel_occupancy(P, st->jokers != 0, st->consecutive != 0, variant, mode, block, smem,
-                                       &per_sm);
-      if (e != cudaSuccess) return cuda_fail(e, "occupancy");
-      d->occupancy[okey] = per_sm;
-    }
+    rc = per_sm_of(variant, smem, &per_sm);
+    if (rc) return rc;
     if (per_sm < 1) return set_err(DVC_E_CONFIG, "kernel cannot launch with this block size");
     grid_full = per_sm * d->num_sms;
   }
@@ -901,7 +917,7 @@ int dvc_set_option(const char *name, int64_t value) {
   if (!name) return set_err(DVC_E_CONFIG, "null option name");
   std::string n(name);
   if (n == "kernel") {
-    if (value != 0 && value != 1) return set_err(DVC_E_CONFIG, "kernel must be 0 (refill) or 1 (naive)");
+    if (value < 0 || value > 2) return set_err(DVC_E_CONFIG, "kernel must be 0 (refill), 1 (naive) or 2 (auto)");
     g_kernel = value;
   } else if (n == "block") {
     if (value < 1 || value > 1024) return set_err(DVC_E_CONFIG, "block must be 1..1024");

@@ -171,8 +171,19 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
     const uint32_t cb = ctr_base(sm.codes[a], kp.node), meta = sm.meta[a];
     Sim<P> S;
     uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, kp);
+#ifdef DVC_NAIVE_PREFETCH
+    // small launches are latency-bound: B_{k+1} does not depend on the state,
+    // so it is generated while step k runs
+    uint2 B = philox_rk(s, cb, kp);
+    for (uint32_t k = 0; st != FINISH && st != VOID; ++k) {
+      const uint2 Bn = philox_rk(s, cb | (k + 1u), kp);
+      st = step_block<P, JOK, CONS, MODE>(S, st, B, k, sm.meta, sm.path, a, kp, kp.path_len);
+      B = Bn;
+    }
+#else
     for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
       st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, cb, sm.meta, sm.path, a, kp);
+#endif
     record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
   flush_hist(sm.hist, kp, P);

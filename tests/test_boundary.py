@@ -123,7 +123,7 @@ def test_options_roundtrip(dvc):
     old = dvc.get_option("block")
     with dvc.options(block=128, kernel=1):
         assert dvc.get_option("block") == 128 and dvc.get_option("kernel") == 1
-    assert dvc.get_option("block") == old and dvc.get_option("kernel") == 0
+    assert dvc.get_option("block") == old and dvc.get_option("kernel") == 2   # auto
     with pytest.raises(dvc.DvcError):
         dvc.set_option("block", 1025)
     with pytest.raises(dvc.DvcError):
