@@ -59,6 +59,7 @@ def lib():
         L.oracle_rollout.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64)]
         L.oracle_rollout_flags.argtypes = [P(I32), P(U32), I32, U64, U32, U64, U64, P(U64), I32]
         L.oracle_playout.argtypes = [P(I32), U32, U64, U32, U32, P(I32)]
+        L.oracle_rollout_fixed.argtypes = [P(I32), P(U32), P(U64), I32, U64, U32, U64, U64, P(U64)]
         L.oracle_rollout_path.argtypes = [P(I32), P(U32), I32, P(U32), I32, U64, U32, U64, U64, P(U64), P(U64)]
         _lib = L
     return _lib
@@ -136,6 +137,18 @@ def rollout(obs_json, codes, seed, node_id, s0, s1, crn=False, informed=False):
     h = (ctypes.c_uint64 * max(A * P, 1))()
     flags = (1 if crn else 0) | (2 if informed else 0)
     _check(lib().oracle_rollout_flags(flatten(obs_json), c, A, seed, node_id, s0, s1, h, flags))
+    return [list(h[a * P:(a + 1) * P]) for a in range(A)]
+
+
+def rollout_fixed(obs_json, codes, rhos, seed, node_id, s0, s1):
+    """The md ablation batch: hist[i][w] for child i =
+    (determinization rhos[i], action codes[i]), sims [s0, s1)."""
+    P = int(obs_json["rules"]["players"])
+    A = len(codes)
+    c = (ctypes.c_uint32 * max(A, 1))(*codes)
+    r = (ctypes.c_uint64 * max(A, 1))(*rhos)
+    h = (ctypes.c_uint64 * max(A * P, 1))()
+    _check(lib().oracle_rollout_fixed(flatten(obs_json), c, r, A, seed, node_id, s0, s1, h))
     return [list(h[a * P:(a + 1) * P]) for a in range(A)]
 
 

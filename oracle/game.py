@@ -474,15 +474,18 @@ class DetSpace:
 
 # ----------------------------------------------------------------- playout (§R5)
 
-def playout(space, code, seed, node_id, s, trace=None, crn=False, informed=False):
+def playout(space, code, seed, node_id, s, trace=None, crn=False, informed=False, rho=None):
     """One playout: determinize with block D, apply the root action, then play
     uniformly random decisions with one Philox2x32 block per decision step
-    (b0: draw, b1: decision; §R3).
+    (b0: draw, b1: decision; §R3).  rho: play determinization rho of Det(O)
+    instead of sampling one (the "md" ablation, §R11).
     Returns the winner seat.  crn: D is keyed by CRN_WORD instead of the code
     (common determinizations across actions); informed: every
     decision is uniform over the order-aware list (§R10) instead of LEGAL."""
-    D = px.det_block(seed, node_id, px.CRN_WORD if crn else code, s)
-    rho = px.rank64(space.N, D[0], D[1])
+    if rho is None:
+        D = px.det_block(seed, node_id, px.CRN_WORD if crn else code, s)
+        rho = px.rank64(space.N, D[0], D[1])
+    # else: the "md" ablation's fixed determinization (DESIGN.md §R11, PAPER:143)
     game = space.game(space.unrank(rho))
     step = game.apply(code)
     k = 0
@@ -550,6 +553,22 @@ def playout_path(space, path, code, seed, node_id, s, trace=None):
 def check_action(obs, code):
     if code not in root_legal(obs):
         raise ValueError("illegal action %08x" % code)
+
+
+def rollout_fixed(obs, codes, rhos, seed, node_id, s0, s1):
+    """The "md" ablation batch (§R11): hist[i][w] for child (rhos[i], codes[i])."""
+    space = DetSpace(obs)
+    if space.N == 0:
+        raise ValueError("inconsistent")
+    for c, r in zip(codes, rhos):
+        check_action(obs, c)
+        if not 0 <= r < space.N:
+            raise ValueError("rho out of range")
+    hist = [[0] * obs.rules.P for _ in codes]
+    for ai, (c, r) in enumerate(zip(codes, rhos)):
+        for s in range(s0, s1):
+            hist[ai][playout(space, c, seed, node_id, s, rho=r)] += 1
+    return hist
 
 
 def rollout(obs, codes, seed, node_id, s0, s1, crn=False, informed=False):

@@ -395,11 +395,18 @@ void root_legal(const Obs &o, std::vector<u32> &out) {
 // crn: D keyed by CRN_WORD instead of the code (common determinizations
 // across actions).
 
+// fixed_rho: the \md ablation -- the playout's
+// determinization is element *fixed_rho of Det(O) instead of rank64(N, D).
 int playout(DetSpace &sp, u32 code, u64 seed, u32 node, u32 s, int *steps,
-            std::vector<u32> &L, bool crn = false, bool informed = false) {
+            std::vector<u32> &L, bool crn = false, bool informed = false, const u64 *fixed_rho = nullptr) {
   const u32 K = stream_key(seed, node);
-  Block D = philox2(s, ctr1(63, crn ? CRN_WORD : code, node), K);
-  u64 rho = rank64(sp.N, D.v[0], D.v[1]);
+  u64 rho;
+  if (fixed_rho) {
+    rho = *fixed_rho;
+  } else {
+    Block D = philox2(s, ctr1(63, crn ? CRN_WORD : code, node), K);
+    rho = rank64(sp.N, D.v[0], D.v[1]);
+  }
   Game G = sp.game(sp.unrank(rho));
   Game::Step st = G.apply(code);
   u32 k = 0;
@@ -516,6 +523,27 @@ int oracle_rollout_flags(const int32_t *obs, const uint32_t *codes, int32_t n_co
       for (u64 s = s0; s < s1; ++s)
         hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L, (flags & 1) != 0,
                                      (flags & 2) != 0)] += 1;
+    return 0;
+  } catch (std::exception &e) { g_err = e.what(); return -1; }
+}
+
+// \md ablation batch: child a = (determinization rhos[a], action codes[a])
+int oracle_rollout_fixed(const int32_t *obs, const uint32_t *codes, const uint64_t *rhos, int32_t n_codes,
+                         uint64_t seed, uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist) {
+  try {
+    Obs o = parse(obs);
+    DetSpace sp(o);
+    if (sp.N == 0) { g_err = "inconsistent"; return -4; }
+    std::vector<u32> L;
+    root_legal(o, L);
+    for (int a = 0; a < n_codes; ++a) {
+      if (std::find(L.begin(), L.end(), codes[a]) == L.end()) { g_err = "illegal action"; return -3; }
+      if (rhos[a] >= sp.N) { g_err = "rho out of range"; return -1; }
+    }
+    int P = o.rules.P;
+    for (int a = 0; a < n_codes; ++a)
+      for (u64 s = s0; s < s1; ++s)
+        hist[(size_t)a * P + playout(sp, codes[a], seed, node, (u32)s, nullptr, L, false, false, rhos + a)] += 1;
     return 0;
   } catch (std::exception &e) { g_err = e.what(); return -1; }
 }
