@@ -165,6 +165,27 @@ int dvc_rollout_batch_flags_async(const dvc_state *s, const uint32_t *actions, i
                                   uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
                                   uint64_t *d_hist, int32_t device, void *cuda_stream);
 
+/* The "md" ablation ("nodes are enriched with
+ * information regarding the chosen set of numbers", the vanilla tree PAPER:145
+ * discards): child a = (determinization rhos[a], action actions[a]).  Every
+ * playout of child a plays the rhos[a]-th element of Det(O) in canonical order
+ * (§R4) instead of sampling one; the rest is dvc_rollout_batch_ex (blocking,
+ * HOST hist[A*P]; actions may repeat with different rhos).  Errors:
+ * DVC_E_CONFIG when rhos is null or some rhos[a] >= N (dvc_state_query's
+ * n_det), plus every error of dvc_rollout_batch_ex. */
+int dvc_rollout_batch_fixed_ex(const dvc_state *s, const uint32_t *actions, const uint64_t *rhos,
+                               int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin,
+                               uint64_t sim_end, uint64_t *hist, int32_t device);
+
+/* SPEC:230 sample_determinization: rhos_out[i] = the element of Det(O)
+ * (canonical order) that sim s_begin + i of a CRN batch
+ * (DVC_FLAG_CRN, seed, node_id) plays, i.e. rank64(N, D) for D the Philox2x32
+ * determinization block of that sim under the CRN word (§R3), i = 0..k-1
+ * (duplicates possible).  Host-side, no device work.  Errors: DVC_E_CONFIG
+ * for a bad state, k < 0, a null buffer or s_begin + k > 2^32. */
+int dvc_sample_determinizations(const dvc_state *s, uint64_t seed, uint32_t node_id, uint32_t s_begin, int32_t k,
+                                uint64_t *rhos_out);
+
 /* Debug/parity form of the async call: additionally writes the winner seat of
  * every playout to d_winners[a*(sim_end-sim_begin) + (s - sim_begin)] (DEVICE,
  * uint8).  Same kernels and launch configuration as the async call. */
@@ -230,6 +251,30 @@ typedef struct {
 typedef struct { uint32_t code, _pad; uint64_t visits, wins; } dvc_action_stat;
 int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table, int32_t cap,
                     int32_t *n_out, uint32_t *best_code);
+
+/* The "md" ablation search (PAPER:143 vanilla tree, discarded
+ * PAPER:145): flat UCT over children (rho_i, a) -- n_det candidate
+ * determinizations x LEGAL.  rho_i: all of Det(O) when N <= n_det, else the
+ * first n_det distinct values of dvc_sample_determinizations(seed, node 0,
+ * sims 0, 1, ...) (at most 64 n_det samples are drawn).  Child j = i*A + a.
+ * The first min(expansions, n_det*A) iterations visit the unvisited children
+ * in index order (one batch per rho_i, node_id = 1 + i, sims [0, n)); later
+ * iterations select the max UCB1 child (unvisited first, ties -> smallest j)
+ * and run sims [visits, visits + n) of it (node_id = 1 + i).  table[a] = the
+ * per-action sums over rho_i of visits and viewer wins in LEGAL order;
+ * *best_code = most visits, then most wins, then smallest code;
+ * *n_det_out = the number of candidate determinizations used. */
+typedef struct {
+  double c;                 /* UCB1 exploration constant                      */
+  int32_t n_det;            /* candidate determinizations (>= 1)              */
+  int32_t expansions;       /* UCB iterations                                 */
+  uint64_t sims_per_child;  /* playouts per iteration                         */
+  uint64_t seed;            /* Philox seed of every batch and of the rho_i    */
+  int32_t device;           /* CUDA ordinal, -1 = current                     */
+  uint32_t _pad;
+} dvc_md_params;
+int dvc_md_search(const dvc_state *s, const dvc_md_params *p, dvc_action_stat *table, int32_t cap,
+                  int32_t *n_out, uint32_t *best_code, int32_t *n_det_out);
 
 /* Debug build only (libdvc_debug.so, compiled with -DDVC_DEBUG): out3 =
  * {invariant violations, code of the first one, finished playouts checked}

@@ -8,7 +8,9 @@ SPEC:240-264.
 
 import math
 
-from . import rollout as oracle_rollout, legal as oracle_legal
+from . import rollout as oracle_rollout, legal as oracle_legal, rollout_fixed as oracle_rollout_fixed, \
+    count as oracle_count
+from . import philox as px
 
 
 LN2 = 0.6931471805599453        # the double nearest ln 2
@@ -148,3 +150,51 @@ def deep_search(obs_json, expansions, sims_per_child, seed, max_depth=4, c=math.
     by_code = {nodes[ch]["code"]: (nodes[ch]["visits"], nodes[ch]["wins"]) for ch in nodes[0]["children"]}
     stats = [(code, by_code.get(code, (0, 0))[0], by_code.get(code, (0, 0))[1]) for code in root_codes]
     return best_child(stats), stats
+
+
+def md_candidates(obs_json, n_det, seed):
+    """The md ablation's candidate determinizations: all of
+    Det(O) when N <= n_det, else the first n_det distinct rho of the CRN
+    determinization blocks of sims 0, 1, ... (node 0), at most 64 n_det draws."""
+    N = oracle_count(obs_json)
+    if N <= n_det:
+        return list(range(N))
+    out = []
+    for s in range(64 * n_det):
+        D = px.det_block(seed, 0, px.CRN_WORD, s)
+        r = px.rank64(N, D[0], D[1])
+        if r not in out:
+            out.append(r)
+            if len(out) == n_det:
+                break
+    return out
+
+
+def md_search(obs_json, n_det, expansions, sims_per_child, seed, c=math.sqrt(2.0)):
+    """The md ablation (PAPER:143 vanilla tree, discarded at
+    PAPER:145): flat UCT over children j = i*A + a = (rho_i, LEGAL[a]); child j's
+    playouts play determinization rho_i with Philox node 1 + i.  Returns
+    (best_code, [(code, visits, wins)] summed over rho_i in LEGAL order, K)."""
+    codes = oracle_legal(obs_json)
+    viewer = obs_json["viewer"]
+    rhos = md_candidates(obs_json, n_det, seed)
+    K, A = len(rhos), len(codes)
+    visits = [0] * (K * A)
+    wins = [0] * (K * A)
+    N = 0
+    for _ in range(expansions):
+        best = None
+        for j in range(K * A):
+            v = ucb1(wins[j], visits[j], N, c)
+            if best is None or v > bv:          # ties -> smallest index
+                best, bv = j, v
+        i, a = divmod(best, A)
+        h = oracle_rollout_fixed(obs_json, [codes[a]], [rhos[i]], seed, 1 + i, visits[best],
+                                 visits[best] + sims_per_child)[0]
+        visits[best] += sims_per_child
+        wins[best] += h[viewer]
+        N += sims_per_child
+    va = [sum(visits[i * A + a] for i in range(K)) for a in range(A)]
+    wa = [sum(wins[i * A + a] for i in range(K)) for a in range(A)]
+    stats = list(zip(codes, va, wa))
+    return best_child(stats), stats, K

@@ -72,6 +72,8 @@ struct HostLane {
   size_t hist_cap = 0;
   unsigned char *d_search = nullptr;     // device flat search: lnN, delta, out, batch_pos
   size_t search_cap = 0;
+  unsigned long long *d_rho = nullptr;   // md ablation batches: per-action determinization (kMaxActions)
+  unsigned long long *h_rho = nullptr;   // pinned staging for its upload
 };
 
 struct DeviceScratch {
@@ -349,6 +351,7 @@ struct BatchOpts {
   unsigned long long *d_voids = nullptr;
   bool crn = false;         // common random numbers across actions (root batches only)
   bool informed = false;    // informed playout policy (root batches only)
+  const unsigned long long *d_rho = nullptr;   // md ablation: fixed determinization per action (§R11)
 };
 
 int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed, uint32_t node_id,
@@ -393,6 +396,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
   kp.hist = d_hist;
   kp.winners = d_winners;
   kp.crn = path.crn ? 1u : 0u;
+  kp.rho = path.d_rho;
   kp.trace_stride = (uint32_t)(sim_end - sim_begin);
   kp.trace_s0 = (uint32_t)sim_begin;
 
@@ -744,7 +748,7 @@ namespace dvc {
 namespace {
 int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                      uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist, uint64_t *visits,
-                     int32_t device, uint32_t flags) {
+                     int32_t device, uint32_t flags, const uint64_t *rhos = nullptr) {
   if (flags & ~(uint32_t)(DVC_FLAG_CRN | DVC_FLAG_INFORMED)) return set_err(DVC_E_CONFIG, "unknown batch flag");
   if (!hist) return set_err(DVC_E_CONFIG, "hist is null");
   const State *st = s ? as_state(s) : nullptr;
@@ -759,6 +763,9 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
     const char *err = nullptr;
     int rc = decode_actions(*st, actions, n_actions, meta.data(), &err);
     if (rc) return set_err(rc, err ? err : "illegal action");
+    if (rhos)
+      for (int32_t a = 0; a < n_actions; ++a)
+        if (rhos[a] >= st->N) return set_err(DVC_E_CONFIG, "rho must be < N (the determinization count)");
   }
   const size_t n = (size_t)n_actions * st->P;
   DeviceScratch *d = nullptr;
@@ -771,10 +778,23 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
     if (rc) return rc;
     cudaError_t e = cudaMemsetAsync(L->d_hist, 0, n * sizeof(unsigned long long), L->stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
+    if (rhos) {
+      if (!L->d_rho) {
+        e = cudaMalloc(&L->d_rho, kMaxActions * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMallocHost(&L->h_rho, kMaxActions * sizeof(unsigned long long));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(rho)");
+      }
+      // the previous call on this lane has completed (blocking calls end with a sync)
+      for (int32_t a = 0; a < n_actions; ++a) L->h_rho[a] = rhos[a];
+      e = cudaMemcpyAsync(L->d_rho, L->h_rho, (size_t)n_actions * sizeof(unsigned long long),
+                          cudaMemcpyHostToDevice, L->stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(rho)");
+    }
   }
   BatchOpts opt;
   opt.crn = (flags & DVC_FLAG_CRN) != 0;
   opt.informed = (flags & DVC_FLAG_INFORMED) != 0;
+  opt.d_rho = rhos ? L->d_rho : nullptr;
   int rc = enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end, L->d_hist, nullptr, d->device,
                    L->stream, nullptr, opt);
   if (rc) return rc;
@@ -823,6 +843,31 @@ int dvc_rollout_batch_flags_ex(const dvc_state *s, const uint32_t *actions, int3
                                uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
                                uint64_t *hist, int32_t device) {
   return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, flags);
+}
+
+int dvc_sample_determinizations(const dvc_state *s, uint64_t seed, uint32_t node_id, uint32_t s_begin, int32_t k,
+                                uint64_t *rhos_out) {
+  const State *st = s ? as_state(s) : nullptr;
+  if (!st) return set_err(DVC_E_CONFIG, "bad state");
+  if (k < 0 || (k > 0 && !rhos_out)) return set_err(DVC_E_CONFIG, "need k >= 0 and an output buffer");
+  if ((uint64_t)s_begin + (uint64_t)k > (1ull << 32)) return set_err(DVC_E_CONFIG, "sim indices are 32-bit");
+  // the determinization block D of sim s under common random numbers (§R3),
+  // rho = rank64(N, d0, d1): the element of Det(O) a CRN batch plays at sim s
+  const uint32_t K = stream_key((uint32_t)seed, (uint32_t)(seed >> 32), node_id);
+  const uint32_t c1 = ctr_base(kCrnWord, node_id) | kDetStep;
+  for (int32_t i = 0; i < k; ++i) {
+    const uint2 D = philox2x32_10(s_begin + (uint32_t)i, c1, K);
+    const unsigned __int128 x = ((unsigned __int128)D.y << 32) | D.x;
+    rhos_out[i] = (uint64_t)((x * st->N) >> 64);
+  }
+  return DVC_OK;
+}
+
+int dvc_rollout_batch_fixed_ex(const dvc_state *s, const uint32_t *actions, const uint64_t *rhos,
+                               int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin,
+                               uint64_t sim_end, uint64_t *hist, int32_t device) {
+  if (!rhos) return set_err(DVC_E_CONFIG, "rhos is null");
+  return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, 0u, rhos);
 }
 
 int dvc_rollout_batch_flags_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
@@ -997,6 +1042,8 @@ void dvc_shutdown(void) {
       if (kv2.second.d_hist) cudaFree(kv2.second.d_hist);
       if (kv2.second.h_hist) cudaFreeHost(kv2.second.h_hist);
       if (kv2.second.d_search) cudaFree(kv2.second.d_search);
+      if (kv2.second.d_rho) cudaFree(kv2.second.d_rho);
+      if (kv2.second.h_rho) cudaFreeHost(kv2.second.h_rho);
       if (kv2.second.stream) cudaStreamDestroy(kv2.second.stream);
     }
     delete d;

@@ -91,12 +91,16 @@ __device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P,
 // Start of playout (a, s): determinization block D, table lookup (a2), root
 // action (a3).  Returns the step state.  cb = ctr_base(code, node) (§R3).
 template <int P, bool JOK, bool CONS, int MODE>
-__device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t cb, uint32_t meta,
+__device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_t cb, uint32_t meta, uint32_t a,
                                                   const KParams &kp) {
   constexpr bool PATH = MODE == kModePath;
-  // cb = ctr_base(code, node); under CRN the D block takes the CRN word's base
-  const uint2 D = philox_rk(s, (kp.crn ? ctr_base(kCrnWord, kp.node) : cb) | kDetStep, kp);
-  determinize<P>(S, D, kp);
+  if (MODE == kModePlain && kp.rho) {
+    determinize_rho<P>(S, kp.rho[a], kp);        // md ablation: the child's own determinization (§R11)
+  } else {
+    // cb = ctr_base(code, node); under CRN the D block takes the CRN word's base
+    const uint2 D = philox_rk(s, (kp.crn ? ctr_base(kCrnWord, kp.node) : cb) | kDetStep, kp);
+    determinize<P>(S, D, kp);
+  }
   uint32_t t;
   bool correct;
   // deep-tree batches apply the path's first action at the root (F[0])
@@ -170,20 +174,9 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
     const uint32_t s = kp.s0 + (w - a * kp.n_per);
     const uint32_t cb = ctr_base(sm.codes[a], kp.node), meta = sm.meta[a];
     Sim<P> S;
-    uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, kp);
-#ifdef DVC_NAIVE_PREFETCH
-    // small launches are latency-bound: B_{k+1} does not depend on the state,
-    // so it is generated while step k runs
-    uint2 B = philox_rk(s, cb, kp);
-    for (uint32_t k = 0; st != FINISH && st != VOID; ++k) {
-      const uint2 Bn = philox_rk(s, cb | (k + 1u), kp);
-      st = step_block<P, JOK, CONS, MODE>(S, st, B, k, sm.meta, sm.path, a, kp, kp.path_len);
-      B = Bn;
-    }
-#else
+    uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, a, kp);
     for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
       st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, cb, sm.meta, sm.path, a, kp);
-#endif
     record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
   flush_hist(sm.hist, kp, P);
@@ -343,7 +336,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
       Sim<P> T;
       uint32_t pst = FINISH;
       if (valid) {
-        pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcb, pmeta, kp);
+        pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcb, pmeta, pa, kp);
         if (pst == FINISH) {                    // decided by the root action alone
           record<MODE>(sm, kp, P, pa, ps, outcome<P, PATH>(T, pst, kp));
           valid = false;
@@ -477,7 +470,7 @@ __global__ void __launch_bounds__(128) flat_search_kernel(const __grid_constant_
       const uint32_t s = sbase + i;
       Sim<P> S;
       constexpr int MODE = INF ? kModeInformed : kModePlain;
-      uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, kp);
+      uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, best, kp);
       // latency-bound loop: B_{k+1} is independent of the state, so it is
       // generated while step k runs
       uint2 B = philox_rk(s, cb, kp);

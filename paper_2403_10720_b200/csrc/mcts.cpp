@@ -259,3 +259,85 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
   }
   return finish(codes, visits, wins, table, best_code);
 }
+
+// ---------------------------------------------------------------------------
+// The "md" ablation: the paper's vanilla tree keys a node by
+// the guess AND the chosen set of plausible numbers -- fan-out up
+// to 11,880 at the root, which is why the paper discards it.  Flat
+// (root-only) UCT over children (rho_i, a); every playout of a child plays its
+// fixed determinization (dvc_rollout_batch_fixed_ex).  Same UCB1 (ln_series),
+// same tie rules and move choice as the flat search above.
+extern "C" int dvc_md_search(const dvc_state *s, const dvc_md_params *p, dvc_action_stat *table, int32_t cap,
+                             int32_t *n_out, uint32_t *best_code, int32_t *n_det_out) {
+  using namespace dvc;
+  if (!s || !p || !n_out) return set_error(DVC_E_CONFIG, "null argument");
+  const State *st = reinterpret_cast<const State *>(s);
+  if (st->magic != kMagic) return set_error(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
+  if (p->expansions < 1 || p->sims_per_child < 1 || p->n_det < 1 || !(p->c >= 0.0))
+    return set_error(DVC_E_CONFIG, "need expansions >= 1, sims_per_child >= 1, n_det >= 1, c >= 0");
+  int32_t A = 0;
+  legal_actions(*st, nullptr, 0, &A);
+  *n_out = A;
+  if (!table || cap < A) return set_error(DVC_E_CAPACITY, "table capacity below the number of root actions");
+  std::vector<uint32_t> codes((size_t)A);
+  legal_actions(*st, codes.data(), A, &A);
+  // candidate determinizations
+  std::vector<uint64_t> rhos;
+  if (st->N <= (uint64_t)p->n_det) {
+    for (uint64_t r = 0; r < st->N; ++r) rhos.push_back(r);
+  } else {
+    const int32_t draws = 64 * p->n_det;
+    std::vector<uint64_t> smp((size_t)draws);
+    int rc = dvc_sample_determinizations(s, p->seed, 0u, 0u, draws, smp.data());
+    if (rc) return rc;
+    for (int32_t i = 0; i < draws && (int32_t)rhos.size() < p->n_det; ++i)
+      if (std::find(rhos.begin(), rhos.end(), smp[i]) == rhos.end()) rhos.push_back(smp[i]);
+  }
+  const int K = (int)rhos.size();
+  if (n_det_out) *n_det_out = K;
+  const size_t C = (size_t)K * A;
+  std::vector<uint64_t> visits(C, 0), wins(C, 0);
+  const uint64_t n = p->sims_per_child;
+  const int P = st->P;
+  uint64_t N = 0;
+  // expansion: the first min(expansions, C) iterations visit children 0, 1, ...
+  // in index order (all unvisited: +inf, ties -> smallest index), independent
+  // of each other -> one batch per rho_i
+  const size_t k = (size_t)p->expansions < C ? (size_t)p->expansions : C;
+  std::vector<uint64_t> h((size_t)A * P), rr((size_t)A);
+  for (int i = 0; (size_t)i * A < k; ++i) {
+    const int m = (int)std::min<size_t>((size_t)A, k - (size_t)i * A);
+    for (int a = 0; a < m; ++a) rr[a] = rhos[i];
+    int rc = dvc_rollout_batch_fixed_ex(s, codes.data(), rr.data(), m, p->seed, 1u + (uint32_t)i, 0, n, h.data(),
+                                        p->device);
+    if (rc) return rc;
+    for (int a = 0; a < m; ++a) {
+      visits[(size_t)i * A + a] = n;
+      wins[(size_t)i * A + a] = h[(size_t)a * P + st->viewer];
+      N += n;
+    }
+  }
+  std::vector<uint64_t> hist((size_t)P);
+  for (int it = (int)k; it < p->expansions; ++it) {
+    size_t best = 0;
+    double best_v = 0.0;
+    for (size_t j = 0; j < C; ++j) {
+      const double v = visits[j] == 0 ? INFINITY : ucb1(wins[j], visits[j], N, p->c);
+      if (j == 0 || v > best_v) { best = j; best_v = v; }       // ties -> smallest index
+    }
+    if (visits[best] + n > (1ull << 32)) return set_error(DVC_E_CONFIG, "a child's sim index range would pass 2^32");
+    const int i = (int)(best / A), a = (int)(best % A);
+    int rc = dvc_rollout_batch_fixed_ex(s, &codes[a], &rhos[i], 1, p->seed, 1u + (uint32_t)i, visits[best],
+                                        visits[best] + n, hist.data(), p->device);
+    if (rc) return rc;
+    visits[best] += n;
+    wins[best] += hist[st->viewer];
+    N += n;
+  }
+  std::vector<uint64_t> va((size_t)A, 0), wa((size_t)A, 0);
+  for (size_t j = 0; j < C; ++j) {
+    va[j % A] += visits[j];
+    wa[j % A] += wins[j];
+  }
+  return finish(codes, va, wa, table, best_code);
+}

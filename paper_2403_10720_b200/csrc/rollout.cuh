@@ -56,6 +56,7 @@ struct KParams {
                           // constant bank as instruction operands (no registers, no adds)
   const uint4 *table;     // N entries (H1, H2, H3, jinfo) or null -> inline unrank
   const uint8_t *plan;    // DetPlanHdr image (inline unrank / table build)
+  const unsigned long long *rho;  // md ablation (§R11): fixed determinization per action, or null
   unsigned long long *hist;  // [A * P] global counters (added to)
   uint8_t *winners;       // optional per-playout winner trace
   uint32_t *counter;      // refill kernel's work counter (zeroed per launch)
@@ -706,8 +707,7 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
 
 // Determinization (a2): state of playout with determinization block D.
 template <int P>
-__device__ __forceinline__ void determinize(Sim<P> &S, uint2 D, const KParams &kp) {
-  const uint64_t rho = rank64(kp.N, D.x, D.y);
+__device__ __forceinline__ void determinize_rho(Sim<P> &S, uint64_t rho, const KParams &kp) {
   const uint4 e = kp.table ? __ldg(kp.table + rho) : unrank(kp.plan, rho);
   S.H[0] = kp.Hv;
   if (P > 1) S.H[1] = e.x;
@@ -722,6 +722,11 @@ __device__ __forceinline__ void determinize(Sim<P> &S, uint2 D, const KParams &k
   S.g = kp.g0;
   S.pend = kp.pend0;
   S.corr = kp.corr0;
+}
+
+template <int P>
+__device__ __forceinline__ void determinize(Sim<P> &S, uint2 D, const KParams &kp) {
+  determinize_rho<P>(S, rank64(kp.N, D.x, D.y), kp);
 }
 
 // The candidate action at the root (a3).  Returns true for STOP; else the

@@ -28,7 +28,8 @@ HIDDEN = 0xFF
 # every symbol include/dvc.h declares
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
            "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async",
-           "dvc_rollout_batch_flags_ex", "dvc_rollout_batch_flags_async", "dvc_mcts_search",
+           "dvc_rollout_batch_flags_ex", "dvc_rollout_batch_flags_async", "dvc_rollout_batch_fixed_ex",
+           "dvc_sample_determinizations", "dvc_mcts_search", "dvc_md_search",
            "dvc_set_option", "dvc_get_option", "dvc_debug_counters", "dvc_launch_count", "dvc_last_error",
            "dvc_shutdown"]
 
@@ -63,6 +64,12 @@ class _SearchParams(ctypes.Structure):
     _fields_ = [("c", ctypes.c_double), ("max_depth", ctypes.c_int32), ("expansions", ctypes.c_int32),
                 ("sims_per_child", ctypes.c_uint64), ("seed", ctypes.c_uint64), ("flat", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("flags", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
+
+
+class _MdParams(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_double), ("n_det", ctypes.c_int32), ("expansions", ctypes.c_int32),
+                ("sims_per_child", ctypes.c_uint64), ("seed", ctypes.c_uint64), ("device", ctypes.c_int32),
+                ("_pad", ctypes.c_uint32)]
 
 
 class _ActionStat(ctypes.Structure):
@@ -101,8 +108,11 @@ def lib():
         L.dvc_rollout_batch_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_trace_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, VP, VP, I32, VP]
         L.dvc_rollout_batch_flags_ex.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, U32, P(U64), I32]
+        L.dvc_rollout_batch_fixed_ex.argtypes = [P(_State), P(U32), P(U64), I32, U64, U32, U64, U64, P(U64), I32]
         L.dvc_rollout_batch_flags_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, U32, VP, I32, VP]
         L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
+        L.dvc_md_search.argtypes = [P(_State), P(_MdParams), P(_ActionStat), I32, P(I32), P(U32), P(I32)]
+        L.dvc_sample_determinizations.argtypes = [P(_State), U64, U32, U32, I32, P(U64)]
         L.dvc_debug_counters.argtypes = [I32, P(U32)]
         L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
         L.dvc_get_option.argtypes = [ctypes.c_char_p, P(I64)]
@@ -228,6 +238,44 @@ def rollout_batch_ex(state, actions, seed, node_id, sim_begin, sim_end, device=-
         _check(lib().dvc_rollout_batch_ex(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                           hp, None, device))
     return hist
+
+
+def rollout_batch_fixed_ex(state, actions, rhos, seed, node_id, sim_begin, sim_end, device=-1):
+    """The md ablation batch (dvc_rollout_batch_fixed_ex):
+    hist[i, w] (numpy uint64) for child i = (determinization rhos[i],
+    action actions[i]) over sims [sim_begin, sim_end) (blocking)."""
+    a, ap = _codes(actions)
+    r = np.ascontiguousarray(np.asarray(rhos, dtype=np.uint64))
+    if len(r) != len(a):
+        raise ValueError("one rho per action")
+    hist = np.zeros((len(a), state.players), dtype=np.uint64)
+    _check(lib().dvc_rollout_batch_fixed_ex(ctypes.byref(state._s), ap, r.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                            len(a), seed, node_id, sim_begin, sim_end,
+                                            hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), device))
+    return hist
+
+
+def sample_determinizations(state, seed, node_id, sim_begin, k):
+    """SPEC:230 sample_determinization: the Det(O) indices (canonical order)
+    that sims [sim_begin, sim_begin + k) of a CRN batch play (numpy uint64)."""
+    out = np.zeros(k, dtype=np.uint64)
+    _check(lib().dvc_sample_determinizations(ctypes.byref(state._s), seed, node_id, sim_begin, k,
+                                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return out
+
+
+def md_search(state, n_det, expansions, sims_per_child, seed, c=2 ** 0.5, device=-1):
+    """The md ablation search (dvc_md_search).  Returns
+    (best_code, [(code, visits, wins)] in LEGAL order, #candidate determinizations)."""
+    p = _MdParams(c=c, n_det=n_det, expansions=expansions, sims_per_child=sims_per_child, seed=seed, device=device)
+    n = ctypes.c_int32()
+    best = ctypes.c_uint32()
+    kd = ctypes.c_int32()
+    cap = max(1, state.info["n_legal"])
+    tab = (_ActionStat * cap)()
+    _check(lib().dvc_md_search(ctypes.byref(state._s), ctypes.byref(p), tab, cap, ctypes.byref(n),
+                               ctypes.byref(best), ctypes.byref(kd)))
+    return best.value, [(t.code, t.visits, t.wins) for t in tab[:n.value]], kd.value
 
 
 def rollout_path_ex(state, path, actions, seed, node_id, sim_begin, sim_end, device=-1):
