@@ -1,0 +1,62 @@
+"""The md ablation: head-to-head self-play
+on C3 rules (2p, 26 tiles with jokers, consecutive) of the paper's simplified
+search (children keyed by the guess alone; flat UCT 64 x 1024) against
+the vanilla tree keyed by (determinization, guess) at the SAME
+playout budget per decision (1024 UCB iterations x 64 playouts), for a few
+candidate-determinization counts.  Seats alternate over the same deals.
+Reports the simplified search's win rate (95% interval) and the md root
+fan-out (K determinizations x A guesses).
+
+    python tools/md_ablation.py [games] > profiles/r01_md_ablation.jsonl
+"""
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    games = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    from paper_2403_10720_b200 import dvc
+    from paper_2403_10720_b200.selfplay import play_games
+    dvc.set_option("search_device", 1)
+    fan = []
+
+    def simplified(obs, s):
+        best, _ = dvc.mcts_search(dvc.encode(obs), 64, 1024, s)
+        return best
+
+    def md(n_det):
+        def search(obs, s):
+            best, table, k = dvc.md_search(dvc.encode(obs), n_det, 1024, 64, s)
+            fan.append(k * len(table))
+            return best
+        return search
+
+    for n_det in (4, 16, 64):
+        A, B = simplified, md(n_det)
+        fan.clear()
+        t0 = time.perf_counter()
+        res = []
+        for half in (0, 1):
+            def search(obs, s, half=half):
+                return (A if obs["viewer"] == half else B)(obs, s)
+            seeds = list(range(3000, 3000 + games // 2))
+            out = play_games(seeds, threads=16, players=2, ranks=12, jokers=1, consecutive=1, per=4,
+                             search=search)
+            res += [1 if g["winner"] == half else 0 for g in out]
+        w = sum(res)
+        p = w / len(res)
+        print(json.dumps({"a": "simplified flat 64x1024", "b": "md n_det=%d, 1024x64" % n_det, "games": len(res),
+                          "a_wins": w, "a_win_rate": round(p, 4), "ci95": round(1.96 * math.sqrt(p * (1 - p) / len(res)), 4),
+                          "md_root_children_mean": round(sum(fan) / max(1, len(fan)), 1),
+                          "md_root_children_max": max(fan) if fan else 0,
+                          "playouts_per_decision": 65536, "s": round(time.perf_counter() - t0, 1)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
