@@ -456,7 +456,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     kp.s0 = (uint32_t)b;
     kp.n_per = (uint32_t)(e_ - b);
     kp.total = kp.n_per * kp.A;
-    kp.nb = (kp.n_per + 31u) / 32u;   // kBatch = 32 (kernels.cu)
+    kp.nb = (kp.n_per + kBatch - 1u) / kBatch;   // refill work batches per action
     // ceil(2^64 / n_per) for the kernels' division-free item -> (action, sim)
     kp.div_magic = kp.n_per == 1 ? 0ull
                  : (uint64_t)(((unsigned __int128)1 << 64) / kp.n_per) + ((((unsigned __int128)1 << 64) % kp.n_per) ? 1 : 0);

@@ -34,7 +34,6 @@ namespace dvc {
 #define DVC_REFILL_MINB 3
 #endif
 
-constexpr uint32_t kBatch = 32;   // sims per work batch of the refill kernel (one produce round)
 
 // Shared memory: hist[A*P] u32 counters, then the action codes and metas
 // (read once per playout start; per-lane indexed, so smem beats the param bank).
