@@ -440,8 +440,8 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
     for (uint32_t is_w = 0; is_w < 2; ++is_w) {
       const bool hidJ = is_w ? hidW : hidB;
       const uint32_t kj = is_w ? kw : kb;
-      const uint32_t pre = below(kj);             // numbered keys left of the joker
-      uint32_t c = nB * __popc(hb & pre) + nW * __popc(hw & pre);
+      // weight of the numbered slots left of the joker (keys below kj)
+      uint32_t c = nB * popc_below(hb, kj) + nW * popc_below(hw, kj);
       const bool hidO = is_w ? hidB : hidW;
       const uint32_t ko = is_w ? kb : kw;
       c += (hidO & joker_first(ji, is_w ^ 1u, ko, kj)) ? (is_w ? nB : nW) : 0u;
