@@ -21,12 +21,12 @@ constexpr int kMaxActions = 768;
 #endif
 constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the refill kernel
 constexpr uint32_t kRingSlots = 64;                          // started playouts per warp
-// 16 B vectors per refill-kernel ring slot (kernels.cu RingView): 12 words for
-// two players (unpacked turn fields), P + 7 packed otherwise.  (Carrying the
+// 16 B vectors per refill-kernel ring slot (kernels.cu RingView): P + 10 words
+// (unpacked turn fields).  (Carrying the
 // next step's Philox block instead, so it could be generated during the
 // current step, measured -7% with Philox4x32 and -0.5..+1% with Philox2x32:
 // not kept.)
-__host__ __device__ constexpr uint32_t ring_vecs(int P) { return P == 2 ? 3u : (uint32_t)(P + 7 + 3) / 4u; }
+__host__ __device__ constexpr uint32_t ring_vecs(int P) { return (uint32_t)(P + 10 + 3) / 4u; }
 
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
 constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's code under common random numbers (no action code, §R3)
