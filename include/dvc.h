@@ -266,7 +266,7 @@ int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_s
  * *n_det_out = the number of candidate determinizations used. */
 typedef struct {
   double c;                 /* UCB1 exploration constant                      */
-  int32_t n_det;            /* candidate determinizations (>= 1)              */
+  int32_t n_det;            /* candidate determinizations (1..4096)           */
   int32_t expansions;       /* UCB iterations                                 */
   uint64_t sims_per_child;  /* playouts per iteration                         */
   uint64_t seed;            /* Philox seed of every batch and of the rho_i    */

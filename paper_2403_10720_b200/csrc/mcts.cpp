@@ -273,8 +273,8 @@ extern "C" int dvc_md_search(const dvc_state *s, const dvc_md_params *p, dvc_act
   if (!s || !p || !n_out) return set_error(DVC_E_CONFIG, "null argument");
   const State *st = reinterpret_cast<const State *>(s);
   if (st->magic != kMagic) return set_error(DVC_E_CONFIG, "state was not produced by dvc_state_encode");
-  if (p->expansions < 1 || p->sims_per_child < 1 || p->n_det < 1 || !(p->c >= 0.0))
-    return set_error(DVC_E_CONFIG, "need expansions >= 1, sims_per_child >= 1, n_det >= 1, c >= 0");
+  if (p->expansions < 1 || p->sims_per_child < 1 || p->n_det < 1 || p->n_det > 4096 || !(p->c >= 0.0))
+    return set_error(DVC_E_CONFIG, "need expansions >= 1, sims_per_child >= 1, 1 <= n_det <= 4096, c >= 0");
   int32_t A = 0;
   legal_actions(*st, nullptr, 0, &A);
   *n_out = A;

@@ -37,3 +37,14 @@ def test_sample_determinizations_errors(dvc):
     with pytest.raises(dvc.DvcError):
         dvc.sample_determinizations(st, 1, 0, (1 << 32) - 10, 11)      # past the 32-bit sim range
     assert len(dvc.sample_determinizations(st, 1, 0, 0, 0)) == 0
+
+
+def test_md_search_argument_errors(dvc):
+    d = json.load(open(os.path.join(ROOT, "fixtures", "c2_d1.json")))
+    st = dvc.encode(d)
+    for bad in (dict(n_det=0), dict(n_det=4097), dict(expansions=0), dict(sims_per_child=0)):
+        kw = dict(n_det=4, expansions=8, sims_per_child=8, seed=1)
+        kw.update(bad)
+        with pytest.raises(dvc.DvcError) as e:
+            dvc.md_search(st, **kw)
+        assert e.value.code == -1
