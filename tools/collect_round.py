@@ -41,7 +41,7 @@ def main():
         if os.path.exists(os.path.join(src, name)):
             shutil.copy(os.path.join(src, name), os.path.join(dst, "%s_%s" % (tag, name.replace("configs.jsonl", "configs_c1_c4.jsonl"))))
     for f in os.listdir(src):
-        if f.endswith(".csv") and f.startswith(tag):
+        if (f.endswith(".csv") or f.endswith(".jsonl")) and f.startswith(tag):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     if os.path.exists(os.path.join(src, "launches_ncu.csv")):
         shutil.copy(os.path.join(src, "launches_ncu.csv"), os.path.join(dst, "%s_launches_ncu.csv" % tag))

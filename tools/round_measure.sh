@@ -8,6 +8,8 @@ set -x
 python tools/configs_bench.py > $O/configs.jsonl 2> $O/configs.err
 python tools/c5_sweep.py --out $O --tag $TAG > $O/c5.log 2>&1
 python tools/paper_experiments.py --out $O --tag $TAG > $O/exp.log 2>&1
+python tools/search_latency.py > $O/r01_search_latency_c3.jsonl 2> $O/sl.err
+python tools/search_latency_deep.py > $O/r01_search_latency_deep.jsonl 2> $O/sld.err
 # launch list of the bench command (cold-cache, serialised; compare shares)
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/plain_bench.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_ncu.csv \
