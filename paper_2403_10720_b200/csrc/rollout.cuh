@@ -488,18 +488,21 @@ __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t w, const KParam
   const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
   uint32_t x = choose(n, w);
   const bool stop = CONS && x >= tot;
-  uint32_t d = 1;
+  // target: the first opponent dd whose cumulative count exceeds x, found by
+  // prefix compares (x >= cnt[1] + ... + cnt[dd-1] for dd = 2..P-1), taking
+  // its hand and the offset into its list on the way
+  uint32_t Hd = S.H[1];
   if (P > 2) {
-    bool found = false;
+    uint32_t pre = cnt[1], sub = 0;
 #pragma unroll
-    for (int dd = 1; dd < P; ++dd) {
-      const bool here = !found && x < cnt[dd];
-      d = here ? (uint32_t)dd : d;
-      x = (!found && !here) ? x - cnt[dd] : x;
-      found = found || here;
+    for (int dd = 2; dd < P; ++dd) {
+      const bool g = x >= pre;
+      Hd = g ? S.H[dd] : Hd;
+      sub = g ? pre : sub;
+      pre += cnt[dd];
     }
+    x -= sub;          // (on STOP x, Hd are unused)
   }
-  const uint32_t Hd = pick<P>(S.H, d);
   uint32_t t, vidx;
   select_slot<JOK>(Hd, S.V, S.ji, nB, nW, x, kp, &t, &vidx);
   *t_out = t;
@@ -621,16 +624,17 @@ __device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t w, con
   const uint32_t n = tot + ((CONS && S.corr) ? 1u : 0u);   // STOP last
   uint32_t x = choose(n, w);
   const bool stop = CONS && x >= tot;
-  uint32_t d = 1;
+  uint32_t Hd = S.H[1];          // target by prefix compares, as in decide()
   if (P > 2) {
-    bool found = false;
+    uint32_t pre = cnt[1], sub = 0;
 #pragma unroll
-    for (int dd = 1; dd < P; ++dd) {
-      const bool here = !found && x < cnt[dd];
-      d = here ? (uint32_t)dd : d;
-      x = (!found && !here) ? x - cnt[dd] : x;
-      found = found || here;
+    for (int dd = 2; dd < P; ++dd) {
+      const bool g = x >= pre;
+      Hd = g ? S.H[dd] : Hd;
+      sub = g ? pre : sub;
+      pre += cnt[dd];
     }
+    x -= sub;
   }
   if (stop) {
     *t_out = kNoKey;
@@ -638,7 +642,7 @@ __device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t w, con
     return true;
   }
   uint32_t t, vidx, win;
-  informed_select<JOK>(c, pick<P>(S.H, d), S.V, S.ji, x, kp, &t, &vidx, &win);
+  informed_select<JOK>(c, Hd, S.V, S.ji, x, kp, &t, &vidx, &win);
   *t_out = t;
   // the slot's list: numbered values of the window ascending, then the joker
   *correct = (JOK && t >= kp.JB) ? vidx == (uint32_t)__popc(win) : vidx == (uint32_t)__popc(win & below(t));
