@@ -197,13 +197,12 @@ template <int P>
 struct RingView {
   // AoS, ring_vecs(P) x 16 B per slot: a pop is 3-4 LDS.128 -- pops run in a
   // divergent region with ~2 lanes, so instructions, not bank conflicts, are
-  // what they cost.  Words: H[P], V, Q, ji, g, pend, corr, st | fi << 4 (turn
-  // fields unpacked: no shifts and masks on a pop), a, s and the playout's
-  // Philox counter word c1 for step 0 (ctr_base(code, node), §R3).  (The
-  // packed form g | pend << 8 | corr << 16 | st << 24 | fi << 28 is kept
-  // below for reference and measurement.)
-  static constexpr bool kUnpacked = true;   // packed fields measured 3.6% (2p) / 1.0% (4p) / 1.4% (3p) slower
-  static constexpr int kNW = kUnpacked ? P + 10 : P + 7;   // words used
+  // what they cost.  Words: H[P], V, Q, ji, g, pend, corr, st | fi << 4, a, s
+  // and the playout's Philox counter word c1 for step 0 (ctr_base(code,
+  // node), §R3).  The turn fields are unpacked -- no shifts and masks on a pop;
+  // packing them into one word (one vector less for 3-4 players) measured
+  // 3.6% (2p), 1.4% (3p) and 1.0% (4p) slower.
+  static constexpr int kNW = P + 10;   // words used
   static constexpr uint32_t V = (kNW + 3) / 4;
   uint4 *base;
   template <bool PATH>
@@ -215,18 +214,13 @@ struct RingView {
     w[P + 0] = S.V;
     w[P + 1] = S.Q;
     w[P + 2] = S.ji;
-    int j = P + 3;
-    if (kUnpacked) {
-      w[j++] = S.g;
-      w[j++] = S.pend;
-      w[j++] = S.corr;
-      w[j++] = PATH ? (st | (S.fi << 4)) : st;   // fi exists in deep-tree batches only
-    } else {
-      w[j++] = S.g | (S.pend << 8) | (S.corr << 16) | (st << 24) | (PATH ? S.fi << 28 : 0u);
-    }
-    w[j++] = a;
-    w[j++] = s;
-    w[j++] = c1;
+    w[P + 3] = S.g;
+    w[P + 4] = S.pend;
+    w[P + 5] = S.corr;
+    w[P + 6] = PATH ? (st | (S.fi << 4)) : st;   // fi exists in deep-tree batches only
+    w[P + 7] = a;
+    w[P + 8] = s;
+    w[P + 9] = c1;
 #pragma unroll
     for (int q = kNW; q < 16; ++q) w[q] = 0;
     uint4 *b = base + V * i;
@@ -248,25 +242,14 @@ struct RingView {
     S.V = w[P + 0];
     S.Q = w[P + 1];
     S.ji = w[P + 2];
-    int j = P + 3;
-    if (kUnpacked) {
-      S.g = w[j++];
-      S.pend = w[j++];
-      S.corr = w[j++];
-      const uint32_t sf = w[j++];
-      st = PATH ? (sf & 0xFu) : sf;          // fi is nonzero in deep-tree batches only
-      S.fi = PATH ? (sf >> 4) : 0u;
-    } else {
-      const uint32_t pk = w[j++];
-      S.g = pk & 0xFFu;
-      S.pend = (pk >> 8) & 0xFFu;
-      S.corr = (pk >> 16) & 0xFFu;
-      st = (pk >> 24) & 0xFu;
-      S.fi = PATH ? pk >> 28 : 0u;
-    }
-    a = w[j++];
-    s = w[j++];
-    c1 = w[j++];
+    S.g = w[P + 3];
+    S.pend = w[P + 4];
+    S.corr = w[P + 5];
+    st = PATH ? (w[P + 6] & 0xFu) : w[P + 6];
+    S.fi = PATH ? (w[P + 6] >> 4) : 0u;
+    a = w[P + 7];
+    s = w[P + 8];
+    c1 = w[P + 9];
   }
 };
 
