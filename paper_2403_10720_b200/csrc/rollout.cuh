@@ -446,10 +446,13 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
       const uint32_t ko = is_w ? kb : kw;
       c += (hidO & joker_first(ji, is_w ^ 1u, ko, kj)) ? (is_w ? nB : nW) : 0u;
       const uint32_t nJ = is_w ? nW : nB;
-      const bool here = hidJ && x >= c && x < c + nJ;
+      // offset of x from the joker's first value: inside its nJ values iff
+      // 0 <= dj < nJ (one unsigned compare), past them iff dj >= nJ (signed)
+      const uint32_t dj = x - c;
+      const bool here = hidJ && dj < nJ;
       sel = here ? kp.JB + is_w : sel;
-      vidx_j = here ? x - c : vidx_j;
-      sub += (hidJ && x >= c + nJ) ? nJ : 0u;
+      vidx_j = here ? dj : vidx_j;
+      sub += (hidJ && (int32_t)dj >= (int32_t)nJ) ? nJ : 0u;
     }
     xs = x - sub;
   }
