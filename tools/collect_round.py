@@ -57,6 +57,12 @@ def main():
             if unit:
                 cmd.append("--unit")
             subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, cwd=ROOT)
+    rep = os.path.join(src, "refill_c2.ncu-rep")
+    summ_json = os.path.join(dst, "%s_refill_c2_ncu.json" % tag)
+    if os.path.exists(rep) and os.path.exists(summ_json):
+        issue = json.load(open(summ_json))["issue_active_pct"]
+        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_opmix.py"), rep,
+                        os.path.join(dst, "%s_refill_c2_opmix.json" % tag), str(issue)], check=True, cwd=ROOT)
     print("collected", tag)
 
 
