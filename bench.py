@@ -315,7 +315,7 @@ def run_product(args):
     A, P = len(codes), st.players
     n = args.sims
     s0, s1 = rank * n, (rank + 1) * n
-    dvc.set_option("kernel", 1 if args.kernel == "naive" else 0)
+    dvc.set_option("kernel", {"refill": 0, "naive": 1, "refill2": 3}[args.kernel])
     dvc.set_option("plan_cache", 0)       # plan upload + det table rebuilt inside every step
     stream = torch.cuda.current_stream()
     hist = torch.zeros((A, P), dtype=torch.int64, device=dev)
@@ -454,7 +454,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--kernel", default="refill", choices=["refill", "naive"])
+    ap.add_argument("--kernel", default="refill", choices=["refill", "naive", "refill2"])
     ap.add_argument("--sims", type=int, default=SIMS_PER_ACTION)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -198,7 +198,11 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
  *                thread-per-playout kernel (the paper-style comparison),
  *                2 = auto (default): naive when all of a call's playouts fit in one
  *                resident wave of naive threads (latency-bound small batches: C1
- *                decisions, search batches), refill otherwise
+ *                decisions, search batches), refill otherwise,
+ *                3 = refill2: the refill kernel with two playouts per lane
+ *                (plain batches; other batch kinds take the refill kernel;
+ *                measured, not the default -- DESIGN.md §M); out of range ->
+ *                DVC_E_CONFIG
  *  "block"       threads per block (1..1024 for the naive kernel; a multiple of
  *                32 up to 256 for the refill kernel; default 128)
  *  "grid"        blocks (0 = auto: resident blocks per SM x #SM, or fewer when

@@ -408,7 +408,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
                                   : kModePlain;
   // hist + codes + meta (+ the refill kernel's per-warp rings of started playouts)
   auto smem_of = [&](int v) {
-    if (v != 0) return ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
+    if (v != 0 && v != 3) return ((size_t)n_actions * (P + 3) + kMaxPath) * sizeof(uint32_t);   // hist[A][P+1], codes, metas, path
     // + the per-warp rings: kRingSlots x ring_vecs(P) x 16 B, 16 B aligned (kernels.cu RingView)
     return (((size_t)n_actions * (P + 3) + kMaxPath + 3) & ~(size_t)3) * sizeof(uint32_t) +
            (size_t)(block / 32) * kRingSlots * ring_vecs(P) * 16;
@@ -438,7 +438,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     variant = total <= (uint64_t)ps * (uint64_t)d->num_sms * (uint64_t)block ? 1 : 0;
   }
   const size_t smem = smem_of(variant);
-  if (variant == 0 && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
+  if ((variant == 0 || variant == 3) && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
   const int grid_opt = (int)g_grid.load();
   int grid_full = grid_opt;
   if (grid_opt <= 0) {
@@ -466,7 +466,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     // refill warp starts 32 playouts at a time; each naive thread plays one)
     int grid = grid_full;
     if (grid_opt <= 0) {
-      const uint64_t per_block = variant == 0 ? (uint64_t)(block / 32) * 32u : (uint64_t)block;
+      const uint64_t per_block = (variant == 0 || variant == 3) ? (uint64_t)(block / 32) * 32u : (uint64_t)block;
       const uint64_t need = ((uint64_t)kp.total + per_block - 1) / per_block;
       if (need < (uint64_t)grid) grid = (int)need;
     }
@@ -962,7 +962,8 @@ int dvc_set_option(const char *name, int64_t value) {
   if (!name) return set_err(DVC_E_CONFIG, "null option name");
   std::string n(name);
   if (n == "kernel") {
-    if (value < 0 || value > 2) return set_err(DVC_E_CONFIG, "kernel must be 0 (refill), 1 (naive) or 2 (auto)");
+    if (value < 0 || value > 3)
+      return set_err(DVC_E_CONFIG, "kernel must be 0 (refill), 1 (naive), 2 (auto) or 3 (refill2: two playouts per lane)");
     g_kernel = value;
   } else if (n == "block") {
     if (value < 1 || value > 1024) return set_err(DVC_E_CONFIG, "block must be 1..1024");
