@@ -200,7 +200,7 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
  *                resident wave of naive threads (latency-bound small batches: C1
  *                decisions, search batches), refill otherwise,
  *                3 = refill2: the refill kernel with two playouts per lane
- *                (plain batches; other batch kinds take the refill kernel;
+ *                (plain batches, block <= 128; other batch kinds take the refill kernel;
  *                measured, not the default -- DESIGN.md §M); out of range ->
  *                DVC_E_CONFIG
  *  "block"       threads per block (1..1024 for the naive kernel; a multiple of

@@ -378,11 +378,11 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
 // stepped too (its result is discarded; plain-mode steps touch no memory) so
 // the two steps stay one basic block.  Results are per playout, so the
 // histogram is identical to the refill kernel's.
-#ifndef DVC_REFILL2_MINB
-#define DVC_REFILL2_MINB 2
+#ifndef DVC_REFILL2_BLOCKS
+#define DVC_REFILL2_BLOCKS 7   // min resident 128-thread blocks per SM: 72 registers (6: 76, -2% C2)
 #endif
 template <int P, bool JOK, bool CONS>
-__global__ void __launch_bounds__(256, DVC_REFILL2_MINB) rollout_refill2_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(128, DVC_REFILL2_BLOCKS) rollout_refill2_kernel(const __grid_constant__ KParams kp) {
   constexpr int MODE = kModePlain;
   const Smem sm = setup_smem(kp, P);
   extern __shared__ uint32_t sh_all[];
