@@ -329,7 +329,12 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
       count += __popc(m);
       __syncwarp();
     }
-    // ---- one decision step for every running lane
+    // ---- two decision steps for every running lane per loop iteration, the
+    // second nested in the first (a lane that finishes in the first idles
+    // through the second): the ballot / pop / produce checks are paid once
+    // per two steps.  DESIGN.md §M: +4.2% C2, +2.4% C4, +6% 2p jokers over one
+    // step; two flat `if (active)` blocks measured +2.8%, three steps 0%,
+    // four -2%.
     if (active) {
       st = step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                           kp.path_len);
@@ -337,6 +342,15 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
       if (st == FINISH || st == VOID) {
         record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
         active = false;
+      }
+      if (active) {
+        st = step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+                                            kp.path_len);
+        ++c1;
+        if (st == FINISH || st == VOID) {
+          record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
+          active = false;
+        }
       }
     }
     // ---- lanes without a playout pop started ones (in the same iteration)
