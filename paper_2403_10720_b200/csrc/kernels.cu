@@ -1,7 +1,7 @@
 // kernels.cu -- the sm_100a kernels of the hot path.
 //
 //  * rollout_refill_kernel (default): persistent, warp-refilling.  Each lane
-//    holds one playout in registers; the loop body is ONE decision step for
+//    holds one playout in registers; the loop body is TWO decision steps for
 //    every active lane.  When lanes finish, __ballot_sync counts them, one
 //    leader atomicAdd on the launch's work counter hands out that many new
 //    (action, sim) items and the lanes start them in the same iteration, so
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
 // applied) in shared memory.  Whenever the ring holds fewer than 32, the whole
 // warp -- converged -- takes 32 new work items and starts them (Philox block D,
 // table lookup, root action), pushing the ones still running.  The main loop is
-// one decision step for every lane; a lane whose playout ends records the
+// two decision steps for every lane; a lane whose playout ends records the
 // winner and pops the next started playout from the ring in the same
 // iteration, so lanes never idle on playout-length variance and the start
 // code never runs with a handful of lanes (BASELINE.json north_star: lanes
