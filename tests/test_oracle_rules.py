@@ -152,10 +152,18 @@ def test_invariant_fuzz(rk):
             L = game.legal()
             n = game.n_choices(L)
             assert n >= 1 and len(L) >= 1
-            # the true tile of every hidden opponent slot is in LEGAL
+            # every action targets a hidden slot of an alive opponent, and the
+            # true tile of every hidden slot of every alive opponent is in LEGAL
             for a in L:
                 j, pos, v = G.decode_action(a)
-                assert not game.lines[j][pos][1]
+                assert j != game.g and game.alive(j) and not game.lines[j][pos][1]
+            Ls = set(L)
+            for j in range(rules.P):
+                if j == game.g or not game.alive(j):
+                    continue
+                for pos, (k, r) in enumerate(game.lines[j]):
+                    if not r:
+                        assert G.action_code(j, pos, k) in Ls
             i = rng.randrange(n)
             a = G.STOP if i == len(L) else L[i]
             st = game.apply(a)
