@@ -141,17 +141,59 @@ def instr_per_playout():
         return None
 
 
+def host_cpu_info():
+    """The host the oracle runs on: CPU model, sockets, physical cores, logical
+    CPUs, and one logical CPU per physical core (the pinning targets)."""
+    model, topo = None, {}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name") and model is None:
+                model = line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    try:
+        allowed = sorted(os.sched_getaffinity(0))
+    except AttributeError:
+        allowed = list(range(os.cpu_count() or 1))
+    for c in allowed:
+        try:
+            base = "/sys/devices/system/cpu/cpu%d/topology/" % c
+            key = (open(base + "physical_package_id").read().strip(), open(base + "core_id").read().strip())
+        except OSError:
+            key = ("0", str(c))
+        topo.setdefault(key, c)
+    pin = sorted(topo.values())
+    return {"model": model, "sockets": len({k[0] for k in topo}), "physical_cores": len(pin),
+            "logical_cpus": os.cpu_count(), "allowed_cpus": len(allowed), "pin_cpus": pin,
+            "oracle_build": "g++ -O2 -std=c++17 -shared -fPIC (scalar, no intrinsics; oracle/__init__.py)"}
+
+
+def _pin_worker(counter, cpus):
+    with counter.get_lock():
+        i = counter.value
+        counter.value += 1
+    try:
+        os.sched_setaffinity(0, {cpus[i % len(cpus)]})
+    except (AttributeError, OSError):
+        pass
+
+
 class OraclePool:
-    """The oracle, as it stands, on the host cores: one process per core over
-    disjoint sim sub-ranges of the same workload (SURVEY §8(d) "all cores")."""
+    """The oracle, as it stands, on the host cores: one process pinned to each
+    physical core (taskset-style sched_setaffinity), disjoint sim sub-ranges of
+    the same workload (SURVEY §8(d) "all cores")."""
 
     def __init__(self, cores=None):
         from concurrent.futures import ProcessPoolExecutor
         import multiprocessing as mp
         import oracle
         oracle.build()
-        self.cores = cores or os.cpu_count() or 1
-        self.ex = ProcessPoolExecutor(max_workers=self.cores, mp_context=mp.get_context("spawn"))
+        self.info = host_cpu_info()
+        cpus = self.info["pin_cpus"]
+        self.cores = cores or len(cpus)
+        ctx = mp.get_context("spawn")
+        self.ex = ProcessPoolExecutor(max_workers=self.cores, mp_context=ctx, initializer=_pin_worker,
+                                      initargs=(ctx.Value("i", 0), cpus))
 
     def calibrate(self, d, codes, seed, budget_s):
         """sims per core so one sample takes about budget_s / 4 of wall time."""
@@ -169,18 +211,43 @@ class OraclePool:
         dt = time.perf_counter() - t0
         n = per_core * self.cores
         playouts = n * len(codes)
-        return {"value": playouts / dt, "unit": UNIT, "cores": self.cores, "kind": "oracle",
-                "sample": "%s, all %d actions x %d sims (%d playouts, %.1f s wall, one oracle process per "
-                          "core over disjoint sim ranges)" % (WORKLOAD, len(codes), n, playouts, dt)}
+        return {"value": playouts / dt, "unit": UNIT, "cores": self.cores, "kind": "oracle", "wall_s": dt,
+                "playouts": playouts,
+                "sample": "%s, all %d actions x %d sims (%d playouts, %.1f s wall, one oracle process pinned to "
+                          "each of %d physical cores, disjoint sim ranges)"
+                          % (WORKLOAD, len(codes), n, playouts, dt, self.cores)}
 
     def close(self):
         self.ex.shutdown()
 
 
+def _one_core_job(args):
+    """SURVEY §8(d) 1-core protocol: one process pinned to one core, the first
+    ceil(1e6 / A) sims of every action (~10^6 playouts), steady clock around
+    the rollout loop (encode and the library load excluded)."""
+    import oracle
+    d, codes, seed, cpu = args
+    try:
+        os.sched_setaffinity(0, {cpu})
+    except (AttributeError, OSError):
+        pass
+    oracle.rollout(d, codes, seed, 0, 0, 1)
+    per = -(-1000000 // len(codes))
+    t0 = time.perf_counter()
+    oracle.rollout(d, codes, seed, 0, 0, per)
+    return per * len(codes), time.perf_counter() - t0
+
+
 def cpu_oracle_baseline(d, codes, seed, budget_s=15.0):
     pool = OraclePool()
     try:
-        return pool.run(d, codes, seed, pool.calibrate(d, codes, seed, budget_s))
+        res = pool.run(d, codes, seed, pool.calibrate(d, codes, seed, budget_s))
+        n1, t1 = pool.ex.submit(_one_core_job, (d, codes, seed, pool.info["pin_cpus"][0])).result()
+        res["one_core"] = {"value": n1 / t1, "unit": UNIT, "playouts": n1, "wall_s": t1,
+                           "sample": "first %d playouts of %s seed %d, one process pinned to cpu %d"
+                                     % (n1, WORKLOAD, seed, pool.info["pin_cpus"][0])}
+        res["host"] = pool.info
+        return res
     finally:
         pool.close()
 
@@ -209,17 +276,21 @@ def run_reference(args):
             times.append(r)
         res = r
     pool.close()
-    vals = [r["value"] for r in times]
-    value = sorted(vals)[len(vals) // 2]
-    ms = 1000.0 * (SIMS_PER_ACTION * len(codes)) / value
+    # value = all timed playouts / all timed wall time; ms_per_step = the
+    # MEASURED wall time of one bounded sample step (not extrapolated to 10^6)
+    wall = sum(r["wall_s"] for r in times)
+    value = sum(r["playouts"] for r in times) / wall
+    ms = 1000.0 * wall / len(times)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": "C2 mid-game root %s, all %d legal actions, bounded oracle sample per step"
-                       % (WORKLOAD, len(codes)), "sims_per_action": SIMS_PER_ACTION,
+                       % (WORKLOAD, len(codes)), "sims_per_action_per_step": per_core * pool.cores,
+                       "playouts_per_step": res["playouts"],
+                       "ms_per_step_note": "measured wall time of one bounded sample step",
                        "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": "oracle",
-                             "sample": res["sample"]},
+                             "sample": res["sample"], "host": pool.info},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -296,6 +367,93 @@ def run_reference_sweep(args):
     return 0
 
 
+# ----------------------------------------------------------------- extra records
+C4_WORKLOAD = "fixtures/c4_d1.json"
+C4_PLAYOUTS_PER_MOVE = 100_000_000
+
+
+def c4_strong_record(args, ws, rank, dev, stream, moves=3, warmup=1):
+    """BASELINE configs[3] (C4: 4 players, 26 tiles, 3 each, 10^8 playouts per
+    move) as STRONG scaling: ceil(1e8 / A) sims per action split over the ws
+    ranks (dist.shard_range), one NCCL all_reduce per move; ms per move = max
+    over ranks of CUDA-event time (kernel + all_reduce).  Rank 0 recomputes
+    the whole move alone and checks the merged histogram bit for bit; the
+    histogram's sha256 must be the same at every N."""
+    import hashlib
+    import torch
+    from paper_2403_10720_b200 import dvc
+    from paper_2403_10720_b200.dist import shard_range
+    d = load_workload(C4_WORKLOAD)
+    st = dvc.encode(d)
+    codes = st.legal_actions()
+    A, P = len(codes), st.players
+    S = -(-C4_PLAYOUTS_PER_MOVE // A)
+    a, b = shard_range(S, rank, ws)
+    hist = torch.zeros((A, P), dtype=torch.int64, device=dev)
+    dvc.set_option("plan_cache", 1)        # the state's table is built once per move in a real search
+    times = []
+    for m in range(warmup + moves):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        hist.zero_()
+        if b > a:
+            dvc.rollout_batch_async(st, codes, 77, 0, a, b, hist, stream=stream)
+        if ws > 1:
+            torch.distributed.all_reduce(hist)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if m >= warmup:
+            times.append(e0.elapsed_time(e1))
+    dvc.set_option("plan_cache", 0)
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t[0])
+    ok = None
+    if rank == 0:
+        full = torch.zeros_like(hist)
+        dvc.rollout_batch_async(st, codes, 77, 0, 0, S, full, stream=stream)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(full, hist))
+    h = hist.cpu()
+    assert int(h.sum()) == A * S
+    return {"workload": "C4 %s (4p, 26 tiles, 3 each, jokers, consecutive)" % C4_WORKLOAD, "actions": A,
+            "sims_per_action": S, "playouts_per_move": A * S, "scaling": "strong", "moves": moves,
+            "ms_per_move": ms, "playouts_per_s": A * S / (ms / 1000.0), "merge_bit_exact": ok,
+            "hist_sha256": hashlib.sha256(h.numpy().tobytes()).hexdigest(),
+            "note": "table cached per move (plan_cache=1); time = kernel + all_reduce, max over ranks"}
+
+
+def c2_deals_record(dvc, torch, dev, stream, n, steps=5):
+    """The headline is one position (c2_d1); the same batch on all eight C2
+    deals (fixtures/c2_d1..8), device time per step, and their mean."""
+    out = {}
+    old_cache = dvc.get_option("plan_cache")
+    dvc.set_option("plan_cache", 1)
+    for k in range(1, 9):
+        path = "fixtures/c2_d%d.json" % k
+        st = dvc.encode(load_workload(path))
+        codes = st.legal_actions()
+        hist = torch.zeros((len(codes), st.players), dtype=torch.int64, device=dev)
+        for w in range(2):
+            dvc.rollout_batch_async(st, codes, 500 + w, 0, 0, n, hist, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(steps):
+            dvc.rollout_batch_async(st, codes, 1 + i, 0, 0, n, hist, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["c2_d%d" % k] = len(codes) * n * steps / (e0.elapsed_time(e1) / 1000.0)
+    dvc.set_option("plan_cache", old_cache)
+    vals = list(out.values())
+    return {"playouts_per_s": out, "mean": sum(vals) / len(vals), "min": min(vals), "max": max(vals),
+            "note": "all legal actions x %d sims per deal, %d steps, device time, plan cached" % (n, steps)}
+
+
 # ----------------------------------------------------------------- product arm
 def run_product(args):
     import torch
@@ -308,6 +466,9 @@ def run_product(args):
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
+        # NCCL INIT logging, so the run's log shows the communicator's rank count
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     d = load_workload()
     st = dvc.encode(d)
@@ -315,7 +476,7 @@ def run_product(args):
     A, P = len(codes), st.players
     n = args.sims
     s0, s1 = rank * n, (rank + 1) * n
-    dvc.set_option("kernel", {"refill": 0, "naive": 1, "refill2": 3}[args.kernel])
+    dvc.set_option("kernel", {"refill": 0, "naive": 1}[args.kernel])
     dvc.set_option("plan_cache", 0)       # plan upload + det table rebuilt inside every step
     stream = torch.cuda.current_stream()
     hist = torch.zeros((A, P), dtype=torch.int64, device=dev)
@@ -369,6 +530,16 @@ def run_product(args):
     playouts_per_step = A * n * ws
     value = playouts_per_step * args.steps / (t_ms / 1000.0)
     assert int(hist.sum()) == playouts_per_step, "histogram does not account for every playout"
+    # a6 check: the last step's merged histogram (seed K, sims [0, ws*n)) must
+    # equal rank 0's recomputation of the whole range alone (keyed Philox +
+    # integer sums: bit-identical for every N)
+    merge_ok = None
+    if rank == 0:
+        full = torch.zeros_like(hist)
+        dvc.rollout_batch_async(st, codes, args.steps, 0, 0, ws * n, full, stream=stream)
+        torch.cuda.synchronize()
+        merge_ok = bool(torch.equal(full, hist))
+    c4 = c4_strong_record(args, ws, rank, dev, stream) if not args.no_c4 else None
 
     # ---- e2e through the public blocking API with host buffers
     e2e = None
@@ -377,6 +548,7 @@ def run_product(args):
         for w in range(2):
             dvc.rollout_batch_ex(dvc.encode(d), codes, 50 + w, 0, s0, s1)
         torch.cuda.synchronize()
+        dvc.transfer_bytes(reset=True)
         t0 = time.perf_counter()
         ke = max(1, args.steps)
         for i in range(ke):
@@ -384,22 +556,29 @@ def run_product(args):
             h = dvc.rollout_batch_ex(st_i, codes, 1 + i, 0, s0, s1)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        xfer = dvc.transfer_bytes()
         assert int(h.sum()) == A * n
-        e2e = {"value": A * n * ke / dt, "unit": UNIT, "h2d_bytes_per_step": 1024 + 8 * A,
-               "d2h_bytes_per_step": 8 * A * P,
-               "path": "dvc.encode + dvc_rollout_batch_ex (host in/out, blocking)"}
+        e2e = {"value": A * n * ke / dt, "unit": UNIT, "h2d_bytes_per_step": xfer[0] // ke,
+               "d2h_bytes_per_step": xfer[1] // ke,
+               "path": "dvc.encode + dvc_rollout_batch_ex (host in/out, blocking)",
+               "bytes_note": "counted by the library (dvc_transfer_bytes): plan image upload + kernel parameter "
+                             "blocks (H2D), histogram readback (D2H)"}
     else:
         from paper_2403_10720_b200 import dist as ddist
         torch.distributed.barrier()
         torch.cuda.synchronize()
+        dvc.transfer_bytes(reset=True)
         t0 = time.perf_counter()
         for i in range(args.steps):
             h = ddist.rollout_batch(dvc.encode(d), codes, n * ws, 1 + i)   # returns host int64 [A, P]
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+        xb = dvc.transfer_bytes()
         e2e = {"value": A * n * ws * args.steps / float(dt[0]), "unit": UNIT,
-               "h2d_bytes_per_step": 1024 + 8 * A, "d2h_bytes_per_step": 8 * A * P,
-               "path": "dvc.encode + dist.rollout_batch (sharded async + NCCL all_reduce + .cpu())"}
+               "h2d_bytes_per_step": xb[0] // args.steps, "d2h_bytes_per_step": xb[1] // args.steps + 8 * A * P,
+               "path": "dvc.encode + dist.rollout_batch (sharded async + NCCL all_reduce + .cpu())",
+               "bytes_note": "rank 0's library-counted H2D (plan image + kernel parameter blocks) and D2H, plus "
+                             "the merged histogram's .cpu() copy"}
 
     if rank == 0:
         pk = peaks()
@@ -426,6 +605,7 @@ def run_product(args):
             roof["frac"] = None
             roof["per_unit"] = "missing profiles/roofline_unit.json"
         roof["kernel_ms"] = k_ms
+        deals = c2_deals_record(dvc, torch, dev, stream, n) if (ws == 1 and not args.no_deals) else None
         cpu = None
         if not args.no_cpu_baseline and ws == 1:
             try:
@@ -441,6 +621,7 @@ def run_product(args):
                            "l2": "flushed between steps (256 MiB write)", "seeds": "1..K",
                            "det_table": "rebuilt every step (plan_cache=0)", "parallelism": "sim-range dp%d" % ws},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "merge_bit_exact": merge_ok, "c4_strong": c4, "c2_deals": deals,
                 "clocks": clk.summary()}
         print(json.dumps(line))
     if ws > 1:
@@ -454,10 +635,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--kernel", default="refill", choices=["refill", "naive", "refill2"])
+    ap.add_argument("--kernel", default="refill", choices=["refill", "naive"])
     ap.add_argument("--sims", type=int, default=SIMS_PER_ACTION)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 strong-scaling record")
+    ap.add_argument("--no-deals", action="store_true", help="skip the 8-deal C2 record")
     ap.add_argument("--ref-sweep", choices=["core1", "exp1", "exp2"], default=None,
                     help="reference arm: the paper's CPU experiment sweeps (tools/paper_experiments.py)")
     ap.add_argument("--ref-sizes", default="1,10,100,1000,10000,100000,1000000")

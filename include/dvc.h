@@ -198,10 +198,7 @@ int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t
  *                thread-per-playout kernel (the paper-style comparison),
  *                2 = auto (default): naive when all of a call's playouts fit in one
  *                resident wave of naive threads (latency-bound small batches: C1
- *                decisions, search batches), refill otherwise,
- *                3 = refill2: the refill kernel with two playouts per lane
- *                (plain batches, block <= 128; other batch kinds take the refill kernel;
- *                measured, not the default -- DESIGN.md §M); out of range ->
+ *                decisions, search batches), refill otherwise; out of range ->
  *                DVC_E_CONFIG
  *  "block"       threads per block (1..1024 for the naive kernel; a multiple of
  *                32 up to 256 for the refill kernel; default 128)
@@ -256,6 +253,28 @@ typedef struct { uint32_t code, _pad; uint64_t visits, wins; } dvc_action_stat;
 int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table, int32_t cap,
                     int32_t *n_out, uint32_t *best_code);
 
+/* The same search with every rollout batch delegated to a caller callback --
+ * root parallelism over ranks (SURVEY §8(e) "the tree replicated on
+ * every rank"): each rank runs this search; its callback plays the rank's
+ * shard of [sim_begin, sim_end) and sums the counts over ranks (dist.py:
+ * all_reduce), so every rank sees identical counts and makes identical UCT
+ * choices.  The UCB1 arithmetic (ln_series, reading #28) and the move choice
+ * stay in this library; the callback only produces counts.
+ *   fn(ctx, path, path_len, actions, n_actions, seed, node_id, sim_begin,
+ *      sim_end, flags, hist, voids) must write into the zeroed HOST arrays
+ *   hist[n_actions * P] (winner histogram) and, when voids != NULL (deep-tree
+ *   batches: path_len >= 1), voids[n_actions], exactly what
+ *   dvc_rollout_path_ex / dvc_rollout_batch_flags_ex would return for the
+ *   whole range, and return 0 (or a DVC_E_* code, which aborts the search
+ *   with that code).  path == NULL for flat batches.  search_device is
+ *   ignored (the tree stays on the host).  fn == NULL -> DVC_E_CONFIG; other
+ *   errors as dvc_mcts_search. */
+typedef int (*dvc_batch_fn)(void *ctx, const uint32_t *path, int32_t path_len, const uint32_t *actions,
+                            int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin,
+                            uint64_t sim_end, uint32_t flags, uint64_t *hist, uint64_t *voids);
+int dvc_mcts_search_cb(const dvc_state *s, const dvc_search_params *p, dvc_batch_fn fn, void *ctx,
+                       dvc_action_stat *table, int32_t cap, int32_t *n_out, uint32_t *best_code);
+
 /* The "md" ablation search (PAPER:143 vanilla tree, discarded
  * PAPER:145): flat UCT over children (rho_i, a) -- n_det candidate
  * determinizations x LEGAL.  rho_i: all of Det(O) when N <= n_det, else the
@@ -285,13 +304,23 @@ int dvc_md_search(const dvc_state *s, const dvc_md_params *p, dvc_action_stat *t
  * accumulated on `device` since its scratch was created (codes: 1 hands/pool
  * not disjoint, 2 tiles not conserved, 3 a pool tile revealed, 4 bad joker
  * threshold, 5 mover dead, 6 too many decisions, 7 not exactly one reveal per
- * guess, 8 STOP without a correct guess, 9 not exactly one survivor).  The
+ * guess, 8 STOP without a correct guess, 9 not exactly one survivor, 10 a pending
+ * (drawn this turn) tile already revealed).  The
  * release library returns DVC_E_CONFIG. */
 int dvc_debug_counters(int32_t device, uint32_t *out3);
 
 /* Number of kernel launches the library enqueued since the last reset
  * (reset = 1 zeroes it); lets callers count GPU launches in a timed region. */
 uint64_t dvc_launch_count(int32_t reset);
+
+/* Bytes the library moved since the last reset (reset = 1 zeroes both after
+ * reading): *h2d = host -> device copies (determinization plan images, md
+ * rho lists, search tables) plus the parameter block of every kernel launch
+ * (the rollout kernel's KParams: codes, metas, round keys); *d2h = device ->
+ * host copies (histograms of the blocking calls, search results).  Copies the
+ * CALLER makes of its own device buffers (the *_async forms) are not counted.
+ * Either pointer may be NULL.  Always DVC_OK. */
+int dvc_transfer_bytes(int32_t reset, uint64_t *h2d, uint64_t *d2h);
 
 const char *dvc_last_error(void);
 void dvc_shutdown(void);

@@ -24,6 +24,7 @@ namespace dvc {
 cudaError_t launch_rollout(const KParams &kp, int P, bool jok, bool cons, int variant, int mode, int grid, int block,
                            size_t smem, cudaStream_t stream);
 cudaError_t launch_table(const uint8_t *plan, uint64_t N, uint4 *out, cudaStream_t stream);
+constexpr size_t kTableArgBytes = sizeof(const uint8_t *) + sizeof(uint64_t) + sizeof(uint4 *);   // det_table_kernel params
 cudaError_t launch_add_u64(unsigned long long *p, uint32_t n, uint64_t v, cudaStream_t stream);
 cudaError_t kernel_occupancy(int P, bool jok, bool cons, int variant, int mode, int block, size_t smem,
                              int *blocks_per_sm);
@@ -40,6 +41,9 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_kernel{2}, g_block{128}, g_grid{0}, g_table_cap{1ll << 26}, g_plan_cache{1},
     g_chunk{1ll << 31}, g_search_device{0};
 std::atomic<uint64_t> g_launches{0};
+// bytes the library moved host -> device (copies + kernel parameter blocks)
+// and device -> host since the last dvc_transfer_bytes(reset = 1)
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
 
 int set_err(int code, const std::string &msg) {
   g_err = msg;
@@ -81,6 +85,10 @@ struct DeviceScratch {
   int num_sms = 0;
   uint32_t *d_counters = nullptr;
   uint32_t next_counter = 0;
+  // per work-counter slot: the event recorded after the last launch that used
+  // it; a launch taking the slot waits on it, so launches on different streams
+  // never share a live slot (> kCounterSlots launches in flight)
+  std::vector<cudaEvent_t> counter_ev;
   uint32_t *d_debug = nullptr;           // DVC_DEBUG builds: invariant counters
   std::unordered_map<std::thread::id, HostLane> lanes;
   std::list<PlanEntry> plans;            // LRU, front = most recent
@@ -92,6 +100,15 @@ struct DeviceScratch {
 
 std::mutex g_mu;
 std::unordered_map<int, DeviceScratch *> g_dev;
+
+// Public entry points select their device (get_scratch -> cudaSetDevice);
+// this restores the caller's current device on return, so a call on device k
+// never changes which device the caller (e.g. torch) is on.
+struct DeviceRestore {
+  int prev = -1;
+  DeviceRestore() { if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; cudaGetLastError(); } }
+  ~DeviceRestore() { if (prev >= 0) cudaSetDevice(prev); }
+};
 
 int cuda_fail(cudaError_t e, const char *where) {
   return set_err(DVC_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -273,9 +290,11 @@ int get_plan(DeviceScratch *d, const State &st, cudaStream_t stream, PlanEntry *
           if (u.first != stream && (e = cudaStreamWaitEvent(stream, u.second, 0)) != cudaSuccess)
             return cuda_fail(e, "cudaStreamWaitEvent(use)");
         e = cudaMemcpyAsync(p.d_plan, p.host_img.data(), p.host_img.size(), cudaMemcpyHostToDevice, stream);
+        g_h2d += p.host_img.size();
         if (e == cudaSuccess && p.d_table) {
           e = launch_table(p.d_plan, p.N, p.d_table, stream);
           g_launches++;
+          g_h2d += kTableArgBytes;
         }
         if (e == cudaSuccess) e = cudaEventRecord(p.ready, stream);
         if (e != cudaSuccess) return cuda_fail(e, "plan rebuild");
@@ -293,12 +312,14 @@ int get_plan(DeviceScratch *d, const State &st, cudaStream_t stream, PlanEntry *
   p.d_plan = static_cast<uint8_t *>(pool_get(d, p.host_img.size(), &p.plan_cap, &e));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(plan)");
   e = cudaMemcpyAsync(p.d_plan, p.host_img.data(), p.host_img.size(), cudaMemcpyHostToDevice, stream);
+  g_h2d += p.host_img.size();
   if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "cudaMemcpyAsync(plan)"); }
   if (p.N <= cap) {
     p.d_table = static_cast<uint4 *>(pool_get(d, p.N * sizeof(uint4), &p.table_cap, &e));
     if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "cudaMalloc(table)"); }
     e = launch_table(p.d_plan, p.N, p.d_table, stream);
     g_launches++;
+    g_h2d += kTableArgBytes;
     if (e != cudaSuccess) { reclaim(d, p); return cuda_fail(e, "det_table_kernel"); }
   }
   e = event_get(d, &p.ready);
@@ -438,7 +459,7 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     variant = total <= (uint64_t)ps * (uint64_t)d->num_sms * (uint64_t)block ? 1 : 0;
   }
   const size_t smem = smem_of(variant);
-  if ((variant == 0 || variant == 3) && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
+  if (variant == 0 && block % 32) return set_err(DVC_E_CONFIG, "the refill kernel needs whole warps (block % 32 == 0)");
   const int grid_opt = (int)g_grid.load();
   int grid_full = grid_opt;
   if (grid_opt <= 0) {
@@ -460,18 +481,31 @@ int enqueue(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint
     // ceil(2^64 / n_per) for the kernels' division-free item -> (action, sim)
     kp.div_magic = kp.n_per == 1 ? 0ull
                  : (uint64_t)(((unsigned __int128)1 << 64) / kp.n_per) + ((((unsigned __int128)1 << 64) % kp.n_per) ? 1 : 0);
-    kp.counter = d->d_counters + 2 * (d->next_counter++ % kCounterSlots);
+    const uint32_t slot = d->next_counter++ % kCounterSlots;
+    kp.counter = d->d_counters + 2 * slot;
     cudaError_t e;
+    if (variant == 0) {
+      if (d->counter_ev.empty()) d->counter_ev.assign(kCounterSlots, nullptr);
+      cudaEvent_t &sev = d->counter_ev[slot];
+      if (sev) {
+        e = cudaStreamWaitEvent(stream, sev, 0);
+      } else {
+        e = cudaEventCreateWithFlags(&sev, cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "work-counter slot");
+    }
     // auto grid: the resident maximum, or fewer blocks for a small launch (each
     // refill warp starts 32 playouts at a time; each naive thread plays one)
     int grid = grid_full;
     if (grid_opt <= 0) {
-      const uint64_t per_block = (variant == 0 || variant == 3) ? (uint64_t)(block / 32) * 32u : (uint64_t)block;
+      const uint64_t per_block = variant == 0 ? (uint64_t)(block / 32) * 32u : (uint64_t)block;
       const uint64_t need = ((uint64_t)kp.total + per_block - 1) / per_block;
       if (need < (uint64_t)grid) grid = (int)need;
     }
     e = launch_rollout(kp, P, st->jokers != 0, st->consecutive != 0, variant, mode, grid, block, smem, stream);
     g_launches++;
+    g_h2d += sizeof(KParams);             // the kernel's parameter block
+    if (e == cudaSuccess && variant == 0) e = cudaEventRecord(d->counter_ev[slot], stream);
     if (e != cudaSuccess) return cuda_fail(e, "rollout kernel launch");
     b = e_;
   }
@@ -603,7 +637,10 @@ int deep_search_gpu_impl(const dvc_state *s, const dvc_search_params *p, const u
   HostLane *L = nullptr;
   std::vector<unsigned long long> out((size_t)2 * A_r);
   int32_t status = 0;
-  std::lock_guard<std::mutex> lock(g_mu);
+  // the lock covers scratch / lane / plan setup, the launch and the async
+  // readbacks; the (long) synchronize below runs without it so other host
+  // threads' calls proceed (the lane and its buffers belong to this thread)
+  std::unique_lock<std::mutex> lock(g_mu);
   rc = get_scratch(p->device, &d);
   if (rc) return rc;
   rc = get_lane(d, 1, &L);
@@ -673,6 +710,7 @@ int deep_search_gpu_impl(const dvc_state *s, const dvc_search_params *p, const u
   if (rc) return rc;
   e = cudaMemcpyAsync(out.data(), da.out, out.size() * 8, cudaMemcpyDeviceToHost, L->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, da.status, 4, cudaMemcpyDeviceToHost, L->stream);
+  lock.unlock();
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "deep search");
   if (da.prof) {
@@ -788,6 +826,7 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
       for (int32_t a = 0; a < n_actions; ++a) L->h_rho[a] = rhos[a];
       e = cudaMemcpyAsync(L->d_rho, L->h_rho, (size_t)n_actions * sizeof(unsigned long long),
                           cudaMemcpyHostToDevice, L->stream);
+      g_h2d += (size_t)n_actions * sizeof(unsigned long long);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(rho)");
     }
   }
@@ -800,6 +839,7 @@ int rollout_blocking(const dvc_state *s, const uint32_t *actions, int32_t n_acti
   if (rc) return rc;
   cudaError_t e = cudaMemcpyAsync(L->h_hist, L->d_hist, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                   L->stream);
+  g_d2h += n * sizeof(unsigned long long);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rollout");
   for (size_t i = 0; i < n; ++i) hist[i] = L->h_hist[i];
@@ -836,17 +876,20 @@ extern "C" {
 int dvc_rollout_batch_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                          uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *hist,
                          uint64_t *visits, int32_t device) {
+  DeviceRestore restore_device;
   return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, visits, device, 0u);
 }
 
 int dvc_rollout_batch_flags_ex(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                                uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
                                uint64_t *hist, int32_t device) {
+  DeviceRestore restore_device;
   return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, flags);
 }
 
 int dvc_sample_determinizations(const dvc_state *s, uint64_t seed, uint32_t node_id, uint32_t s_begin, int32_t k,
                                 uint64_t *rhos_out) {
+  DeviceRestore restore_device;
   const State *st = s ? as_state(s) : nullptr;
   if (!st) return set_err(DVC_E_CONFIG, "bad state");
   if (k < 0 || (k > 0 && !rhos_out)) return set_err(DVC_E_CONFIG, "need k >= 0 and an output buffer");
@@ -866,6 +909,7 @@ int dvc_sample_determinizations(const dvc_state *s, uint64_t seed, uint32_t node
 int dvc_rollout_batch_fixed_ex(const dvc_state *s, const uint32_t *actions, const uint64_t *rhos,
                                int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin,
                                uint64_t sim_end, uint64_t *hist, int32_t device) {
+  DeviceRestore restore_device;
   if (!rhos) return set_err(DVC_E_CONFIG, "rhos is null");
   return rollout_blocking(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device, 0u, rhos);
 }
@@ -873,6 +917,7 @@ int dvc_rollout_batch_fixed_ex(const dvc_state *s, const uint32_t *actions, cons
 int dvc_rollout_batch_flags_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                                   uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint32_t flags,
                                   uint64_t *d_hist, int32_t device, void *cuda_stream) {
+  DeviceRestore restore_device;
   return rollout_async(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d_hist, nullptr, device,
                        cuda_stream, flags);
 }
@@ -880,6 +925,7 @@ int dvc_rollout_batch_flags_async(const dvc_state *s, const uint32_t *actions, i
 int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_len, const uint32_t *actions,
                         int32_t n_actions, uint64_t seed, uint32_t node_id, uint64_t sim_begin, uint64_t sim_end,
                         uint64_t *hist, uint64_t *voids, int32_t device) {
+  DeviceRestore restore_device;
   if (path_len == 0) {
     int rc = dvc_rollout_batch_ex(s, actions, n_actions, seed, node_id, sim_begin, sim_end, hist, nullptr, device);
     if (rc == DVC_OK && voids)
@@ -921,6 +967,7 @@ int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_l
   if (rc) return rc;
   cudaError_t e = cudaMemcpyAsync(L->h_hist, L->d_hist, (n + n_actions) * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, L->stream);
+  g_d2h += (n + n_actions) * sizeof(unsigned long long);
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e != cudaSuccess) return cuda_fail(e, "rollout");
   for (size_t i = 0; i < n; ++i) hist[i] = L->h_hist[i];
@@ -931,6 +978,7 @@ int dvc_rollout_path_ex(const dvc_state *s, const uint32_t *path, int32_t path_l
 
 int dvc_rollout_batch(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t n_sims,
                       uint64_t seed, uint64_t *wins) {
+  DeviceRestore restore_device;
   const State *st = s ? as_state(s) : nullptr;
   if (!st || !wins) return set_err(DVC_E_CONFIG, "bad arguments");
   if (n_sims == 0 || n_sims >= (1ull << 32)) return set_err(DVC_E_CONFIG, "n_sims must be in [1, 2^32)");
@@ -945,6 +993,7 @@ int dvc_rollout_batch(const dvc_state *s, const uint32_t *actions, int32_t n_act
 int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
                             uint64_t *d_visits, int32_t device, void *cuda_stream) {
+  DeviceRestore restore_device;
   return rollout_async(s, actions, n_actions, seed, node_id, sim_begin, sim_end, d_hist, d_visits, device,
                        cuda_stream, 0u);
 }
@@ -952,6 +1001,7 @@ int dvc_rollout_batch_async(const dvc_state *s, const uint32_t *actions, int32_t
 int dvc_rollout_trace_async(const dvc_state *s, const uint32_t *actions, int32_t n_actions, uint64_t seed,
                             uint32_t node_id, uint64_t sim_begin, uint64_t sim_end, uint64_t *d_hist,
                             uint8_t *d_winners, int32_t device, void *cuda_stream) {
+  DeviceRestore restore_device;
   if (!d_hist || !d_winners) return set_err(DVC_E_CONFIG, "null device pointer");
   return enqueue(s, actions, n_actions, seed, node_id, sim_begin, sim_end,
                  reinterpret_cast<unsigned long long *>(d_hist), d_winners, device,
@@ -962,8 +1012,7 @@ int dvc_set_option(const char *name, int64_t value) {
   if (!name) return set_err(DVC_E_CONFIG, "null option name");
   std::string n(name);
   if (n == "kernel") {
-    if (value < 0 || value > 3)
-      return set_err(DVC_E_CONFIG, "kernel must be 0 (refill), 1 (naive), 2 (auto) or 3 (refill2: two playouts per lane)");
+    if (value < 0 || value > 2) return set_err(DVC_E_CONFIG, "kernel must be 0 (refill), 1 (naive) or 2 (auto)");
     g_kernel = value;
   } else if (n == "block") {
     if (value < 1 || value > 1024) return set_err(DVC_E_CONFIG, "block must be 1..1024");
@@ -1004,6 +1053,7 @@ int dvc_get_option(const char *name, int64_t *value) {
 }
 
 int dvc_debug_counters(int32_t device, uint32_t *out3) {
+  DeviceRestore restore_device;
 #ifdef DVC_DEBUG
   if (!out3) return set_err(DVC_E_CONFIG, "null argument");
   std::lock_guard<std::mutex> lock(g_mu);
@@ -1018,6 +1068,13 @@ int dvc_debug_counters(int32_t device, uint32_t *out3) {
   (void)device; (void)out3;
   return set_err(DVC_E_CONFIG, "not a DVC_DEBUG build (libdvc_debug.so has the invariant checks)");
 #endif
+}
+
+int dvc_transfer_bytes(int32_t reset, uint64_t *h2d, uint64_t *d2h) {
+  if (h2d) *h2d = g_h2d.load();
+  if (d2h) *d2h = g_d2h.load();
+  if (reset) { g_h2d = 0; g_d2h = 0; }
+  return DVC_OK;
 }
 
 uint64_t dvc_launch_count(int32_t reset) {
@@ -1038,6 +1095,7 @@ void dvc_shutdown(void) {
     for (auto &p : d->zombies) free_plan_now(p);
     for (auto &b : d->pool) cudaFree(b.first);
     for (auto ev : d->events) cudaEventDestroy(ev);
+    for (auto ev : d->counter_ev) if (ev) cudaEventDestroy(ev);
     if (d->d_counters) cudaFree(d->d_counters);
     for (auto &kv2 : d->lanes) {
       if (kv2.second.d_hist) cudaFree(kv2.second.d_hist);

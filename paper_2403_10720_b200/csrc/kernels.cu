@@ -119,6 +119,7 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
   dbg_check_state<P, JOK>(S, kp);
   if (!(S.H[0] & ~S.V)) dbg_fail(kp, 5);                       // the mover is alive
   if (k >= 2u * (uint32_t)__popc(kp.T)) dbg_fail(kp, 6);        // decisions <= 2(|T|-1)
+  if (S.pend != kNoKey && ((S.V >> S.pend) & 1u)) dbg_fail(kp, 10);   // a pending tile is hidden
   const uint32_t v_before = __popc(S.V);
 #endif
   uint32_t t;
@@ -375,131 +376,6 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
   // The last block out re-arms the work counter (counter[0]) and its exit
   // count (counter[1]) for the launch that reuses this slot, so no launch
   // needs a memset first.  Every block stopped claiming before it counts out.
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(kp.counter + 1, 1u) == gridDim.x - 1u) {
-      atomicExch(kp.counter, 0u);
-      atomicExch(kp.counter + 1, 0u);
-    }
-  }
-}
-
-// ---- refill2 (kernel option 3, plain batches): two playouts per lane ------
-// The refill kernel with two running slots per lane, stepped in the same loop
-// iteration without a branch between them, so the two dependency chains of a
-// decision step (Philox rounds, the 5-step probes) interleave -- ILP instead
-// of more warps (DESIGN.md §M "where the next gains are").  An idle slot is
-// stepped too (its result is discarded; plain-mode steps touch no memory) so
-// the two steps stay one basic block.  Results are per playout, so the
-// histogram is identical to the refill kernel's.
-#ifndef DVC_REFILL2_BLOCKS
-#define DVC_REFILL2_BLOCKS 7   // min resident 128-thread blocks per SM: 72 registers (6: 76, -2% C2)
-#endif
-template <int P, bool JOK, bool CONS>
-__global__ void __launch_bounds__(128, DVC_REFILL2_BLOCKS) rollout_refill2_kernel(const __grid_constant__ KParams kp) {
-  constexpr int MODE = kModePlain;
-  const Smem sm = setup_smem(kp, P);
-  extern __shared__ uint32_t sh_all[];
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * RingView<P>::V * kRing};
-  uint32_t ca = 0, cs = 0, ce = 0, ccb = 0, cmeta = 0;
-  bool drained = false;
-  const uint32_t n_batches = kp.A * kp.nb;
-  uint32_t pref = 0;
-  if (lane == 0) pref = atomicAdd(kp.counter, 1u);
-  uint32_t head = 0, count = 0;
-  bool act0 = false, act1 = false;
-  uint32_t a0 = 0, s0 = 0, st0 = FINISH, c0 = 0;
-  uint32_t a1 = 0, s1 = 0, st1 = FINISH, c1 = 0;
-  Sim<P> S0{}, S1{};
-  while (true) {
-    while (count < 32u && !(drained && cs >= ce)) {
-      uint32_t rem = ce - cs;
-      uint32_t na = 0, ns = 0, ne = 0, ncb = 0, nmeta = 0;
-      bool got = false;
-      if (rem < 32u && !drained) {
-        const uint32_t b = __shfl_sync(0xFFFFFFFFu, pref, 0);
-        if (b < n_batches) {
-          if (lane == 0) pref = atomicAdd(kp.counter, 1u);
-          na = b / kp.nb;
-          ns = (b - na * kp.nb) * kBatch;
-          ne = min(ns + kBatch, kp.n_per);
-          ncb = ctr_base(sm.codes[na], kp.node);
-          nmeta = sm.meta[na];
-          got = true;
-        } else {
-          drained = true;
-        }
-      }
-      bool valid = false;
-      uint32_t pa = 0, ps = 0, pcb = 0, pmeta = 0;
-      if (lane < rem) {
-        pa = ca; ps = kp.s0 + cs + lane; pcb = ccb; pmeta = cmeta; valid = true;
-      } else if (got && ns + (lane - rem) < ne) {
-        pa = na; ps = kp.s0 + ns + (lane - rem); pcb = ncb; pmeta = nmeta; valid = true;
-      }
-      if (got) {
-        ca = na; ccb = ncb; cmeta = nmeta; ce = ne;
-        cs = min(ns + (32u - rem), ne);
-      } else {
-        cs = min(cs + 32u, ce);
-      }
-      Sim<P> T;
-      uint32_t pst = FINISH;
-      if (valid) {
-        pst = start_playout<P, JOK, CONS, MODE>(T, ps, pcb, pmeta, pa, kp);
-        if (pst == FINISH) {
-          record<MODE>(sm, kp, P, pa, ps, outcome<P, false>(T, pst, kp));
-          valid = false;
-        }
-      }
-      const uint32_t m = __ballot_sync(0xFFFFFFFFu, valid);
-      if (valid) ring.template put<false>((head + count + __popc(m & lt_mask)) & (kRing - 1u), T, pst, pa, ps, pcb);
-      count += __popc(m);
-      __syncwarp();
-    }
-    // ---- one decision step for both slots of every lane, one basic block
-    {
-      const uint32_t n0 = step_block<P, JOK, CONS, MODE>(S0, st0, philox_rk(s0, c0, kp), c0 & 63u, sm.meta, sm.path,
-                                                         a0, kp, 0u);
-      const uint32_t n1 = step_block<P, JOK, CONS, MODE>(S1, st1, philox_rk(s1, c1, kp), c1 & 63u, sm.meta, sm.path,
-                                                         a1, kp, 0u);
-      ++c0; ++c1;
-      st0 = n0; st1 = n1;
-      const bool f0 = act0 && n0 == FINISH, f1 = act1 && n1 == FINISH;
-      if (f0) record<MODE>(sm, kp, P, a0, s0, winner_seat(S0));
-      if (f1) record<MODE>(sm, kp, P, a1, s1, winner_seat(S1));
-      act0 = act0 && !f0;
-      act1 = act1 && !f1;
-    }
-    // ---- idle slots pop started playouts: slot 0 first, then slot 1
-    const uint32_t need0 = __ballot_sync(0xFFFFFFFFu, !act0);
-    const uint32_t need1 = __ballot_sync(0xFFFFFFFFu, !act1);
-    if (need0 | need1) {
-      const uint32_t t0 = min((uint32_t)__popc(need0), count);
-      if (t0) {
-        if (!act0 && __popc(need0 & lt_mask) < t0) {
-          ring.template get<false>((head + __popc(need0 & lt_mask)) & (kRing - 1u), S0, st0, a0, s0, c0);
-          act0 = true;
-        }
-        head = (head + t0) & (kRing - 1u);
-        count -= t0;
-      }
-      const uint32_t t1 = min((uint32_t)__popc(need1), count);
-      if (t1) {
-        if (!act1 && __popc(need1 & lt_mask) < t1) {
-          ring.template get<false>((head + __popc(need1 & lt_mask)) & (kRing - 1u), S1, st1, a1, s1, c1);
-          act1 = true;
-        }
-        head = (head + t1) & (kRing - 1u);
-        count -= t1;
-      }
-      __syncwarp();
-      if (count == 0 && drained && cs >= ce && !__any_sync(0xFFFFFFFFu, act0 || act1)) break;
-    }
-  }
-  flush_hist(sm.hist, kp, P);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(kp.counter + 1, 1u) == gridDim.x - 1u) {
@@ -979,10 +855,6 @@ typedef void (*KernelFn)(const KParams);
 
 template <int P, bool JOK, bool CONS, int MODE>
 KernelFn pick_mode(int variant) {
-  if (variant == 3) {
-    if constexpr (MODE == kModePlain) return rollout_refill2_kernel<P, JOK, CONS>;
-    return rollout_refill_kernel<P, JOK, CONS, MODE>;
-  }
   return variant == 1 ? rollout_naive_kernel<P, JOK, CONS, MODE> : rollout_refill_kernel<P, JOK, CONS, MODE>;
 }
 

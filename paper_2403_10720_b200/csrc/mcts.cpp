@@ -11,9 +11,6 @@
 
 #include "dvc_internal.h"
 
-extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table,
-                               int32_t cap, int32_t *n_out, uint32_t *best_code);
-
 namespace {
 
 using namespace dvc;
@@ -31,6 +28,30 @@ struct Node {
   uint64_t visits = 0, wins = 0, tried = 0;
   bool expanded = false;
   std::vector<int32_t> children;
+};
+
+// Where a search's rollout batches run: this process's GPU (the default), or
+// a caller callback that shards the sim range over ranks and sums the counts
+// (dvc_mcts_search_cb; dist.mcts_search).  The UCT arithmetic stays here.
+struct Batcher {
+  dvc_batch_fn fn = nullptr;
+  void *ctx = nullptr;
+  int flat(const dvc_state *s, const uint32_t *codes, int32_t n, uint64_t seed, uint32_t node, uint64_t s0,
+           uint64_t s1, uint32_t flags, uint64_t *hist, int32_t device) const {
+    if (!fn) return dvc_rollout_batch_flags_ex(s, codes, n, seed, node, s0, s1, flags, hist, device);
+    std::fill(hist, hist + (size_t)n * reinterpret_cast<const dvc::State *>(s)->P, 0ull);
+    const int rc = fn(ctx, nullptr, 0, codes, n, seed, node, s0, s1, flags, hist, nullptr);
+    return rc ? dvc::set_error(rc < 0 ? rc : DVC_E_CONFIG, "batch callback failed") : DVC_OK;
+  }
+  int path(const dvc_state *s, const uint32_t *path, int32_t path_len, const uint32_t *codes, int32_t n,
+           uint64_t seed, uint32_t node, uint64_t s0, uint64_t s1, uint64_t *hist, uint64_t *voids,
+           int32_t device) const {
+    if (!fn) return dvc_rollout_path_ex(s, path, path_len, codes, n, seed, node, s0, s1, hist, voids, device);
+    std::fill(hist, hist + (size_t)n * reinterpret_cast<const dvc::State *>(s)->P, 0ull);
+    std::fill(voids, voids + n, 0ull);
+    const int rc = fn(ctx, path, path_len, codes, n, seed, node, s0, s1, 0u, hist, voids);
+    return rc ? dvc::set_error(rc < 0 ? rc : DVC_E_CONFIG, "batch callback failed") : DVC_OK;
+  }
 };
 
 }  // namespace
@@ -62,7 +83,7 @@ double ucb1(uint64_t w, uint64_t v, uint64_t parent, double c) {
 }
 
 int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p, std::vector<uint32_t> &root_codes,
-                std::vector<uint64_t> &rv, std::vector<uint64_t> &rw) {
+                std::vector<uint64_t> &rv, std::vector<uint64_t> &rw, const Batcher &B) {
   if (p->max_depth < 1 || p->max_depth > kMaxPath)
     return set_error(DVC_E_CONFIG, "max_depth must be 1..8 for the deep tree");
   const uint64_t n = p->sims_per_child;
@@ -71,7 +92,7 @@ int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p,
   std::vector<uint32_t> deep_codes;
   for (uint32_t c : root_codes) if (c != DVC_STOP) deep_codes.push_back(c);
   if (st->consecutive) deep_codes.push_back(DVC_STOP);
-  if (search_on_device()) {
+  if (!B.fn && search_on_device()) {
     // the same tree, iterations and batches in one cooperative GPU kernel
     rv.assign(root_codes.size(), 0);
     rw.assign(root_codes.size(), 0);
@@ -126,8 +147,8 @@ int deep_search(const dvc_state *s, const State *st, const dvc_search_params *p,
     if (s0 + n > (1ull << 32)) return set_error(DVC_E_CONFIG, "a node's sim index range would pass 2^32");
     hist.assign(batch.size() * (size_t)P, 0);
     voids.assign(batch.size(), 0);
-    int rc = dvc_rollout_path_ex(s, prefix.data(), (int32_t)prefix.size(), batch.data(), (int32_t)batch.size(),
-                                 p->seed, node_word, s0, s0 + n, hist.data(), voids.data(), p->device);
+    int rc = B.path(s, prefix.data(), (int32_t)prefix.size(), batch.data(), (int32_t)batch.size(), p->seed,
+                    node_word, s0, s0 + n, hist.data(), voids.data(), p->device);
     if (rc) return rc;
     // ---- backpropagation
     uint64_t dv = 0, dw = 0;
@@ -172,8 +193,9 @@ int finish(const std::vector<uint32_t> &codes, const std::vector<uint64_t> &visi
 
 }  // namespace
 
-extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table,
-                               int32_t cap, int32_t *n_out, uint32_t *best_code) {
+namespace {
+int mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table, int32_t cap,
+                int32_t *n_out, uint32_t *best_code, const Batcher &B) {
   using namespace dvc;
   if (!s || !p || !n_out) return set_error(DVC_E_CONFIG, "null argument");
   const State *st = reinterpret_cast<const State *>(s);
@@ -195,7 +217,7 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
   const uint64_t n = p->sims_per_child;
   int it = 0;
   if (!p->flat) {
-    int rc = deep_search(s, st, p, codes, visits, wins);
+    int rc = deep_search(s, st, p, codes, visits, wins, B);
     if (rc) return rc;
     it = p->expansions;
   } else {
@@ -210,7 +232,7 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     std::vector<uint32_t> first((size_t)k);
     for (int i = 0; i < k; ++i) first[i] = codes[order[i]];
     const int iters = p->expansions - k;
-    if (iters > 0 && search_on_device() && n * (uint64_t)(iters + 1) <= (1ull << 32)) {
+    if (iters > 0 && !B.fn && search_on_device() && n * (uint64_t)(iters + 1) <= (1ull << 32)) {
       // The whole search on the GPU (api.cu flat_search_gpu): the same
       // selections and playouts as the host loop below, without a host round
       // trip per iteration.  ln(N) = ln_series((k + it) n), N known in advance.
@@ -224,7 +246,7 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
       return finish(codes, visits, wins, table, best_code);
     }
     std::vector<uint64_t> h((size_t)k * st->P);
-    int rc = dvc_rollout_batch_flags_ex(s, first.data(), k, p->seed, 0u, 0, n, p->flags, h.data(), p->device);
+    int rc = B.flat(s, first.data(), k, p->seed, 0u, 0, n, p->flags, h.data(), p->device);
     if (rc) return rc;
     for (int i = 0; i < k; ++i) {
       visits[order[i]] = n;
@@ -249,8 +271,8 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     if (visits[best] + n > (1ull << 32))
       return set_error(DVC_E_CONFIG, "a child's sim index range would pass 2^32");
     // simulation on the GPU: sims [visits, visits + n) of the chosen child
-    int rc = dvc_rollout_batch_flags_ex(s, &codes[best], 1, p->seed, 0u, visits[best], visits[best] + n, p->flags,
-                                        hist.data(), p->device);
+    int rc = B.flat(s, &codes[best], 1, p->seed, 0u, visits[best], visits[best] + n, p->flags, hist.data(),
+                    p->device);
     if (rc) return rc;
     // backpropagation
     visits[best] += n;
@@ -258,6 +280,21 @@ extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, d
     N += n;
   }
   return finish(codes, visits, wins, table, best_code);
+}
+}  // namespace
+
+extern "C" int dvc_mcts_search(const dvc_state *s, const dvc_search_params *p, dvc_action_stat *table,
+                               int32_t cap, int32_t *n_out, uint32_t *best_code) {
+  return mcts_search(s, p, table, cap, n_out, best_code, Batcher{});
+}
+
+extern "C" int dvc_mcts_search_cb(const dvc_state *s, const dvc_search_params *p, dvc_batch_fn fn, void *ctx,
+                                  dvc_action_stat *table, int32_t cap, int32_t *n_out, uint32_t *best_code) {
+  if (!fn) return dvc::set_error(DVC_E_CONFIG, "null batch callback");
+  Batcher B;
+  B.fn = fn;
+  B.ctx = ctx;
+  return mcts_search(s, p, table, cap, n_out, best_code, B);
 }
 
 // ---------------------------------------------------------------------------

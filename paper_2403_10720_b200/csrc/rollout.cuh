@@ -20,6 +20,9 @@ constexpr int kMaxActions = 768;
 #define DVC_KBATCH 64   // 64: +1.3% on C2 over 32 (half the work-counter atomics), C4 unchanged; 128 no better
 #endif
 constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the refill kernel
+#ifndef DVC_PEND_FAST
+#define DVC_PEND_FAST 1   // a pending (drawn this turn) tile is always hidden: no V test
+#endif
 constexpr uint32_t kRingSlots = 64;                          // started playouts per warp
 // 16 B vectors per refill-kernel ring slot (kernels.cu RingView): P + 10 words
 // (unpacked turn fields).  (Carrying the
@@ -56,8 +59,9 @@ struct KParams {
   uint64_t div_magic;     // ceil(2^64 / n_per) (0 when n_per == 1): item / n_per = umul64hi(item, magic)
   uint32_t nb;            // refill kernel: kBatch-sized sim batches per action = ceil(n_per / kBatch)
   uint32_t crn;           // 1: determinization block keyed by kCrnWord, not the action code (§R3 CRN)
-  uint32_t rk[10];        // Philox2x32 round keys K(seed, node) + r*W, r = 0..9: read from the
-                          // constant bank as instruction operands (no registers, no adds)
+  uint32_t rk[10];        // Philox2x32 round keys K(seed, node) + r*W, r = 0..9, precomputed on
+                          // the host (sm_100a takes no constant-bank ALU operands: one LDC.64
+                          // per key pair per step, no adds)
   const uint4 *table;     // N entries (H1, H2, H3, jinfo) or null -> inline unrank
   const uint8_t *plan;    // DetPlanHdr image (inline unrank / table build)
   const unsigned long long *rho;  // md ablation (§R11): fixed determinization per action, or null
@@ -388,12 +392,26 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
   S.corr = et ? 0u : S.corr;
 }
 
+// Is the mover's tile drawn this turn still hidden?  Only the mover guesses
+// during its turn and its one self-reveal (a wrong guess) ends the turn, and
+// the root's pending tile is hidden by encode's validation -- so a pending
+// tile is always hidden and the test is pend != NONE (the debug build checks
+// the invariant, code 10).
+template <int P>
+__device__ __forceinline__ bool pending_hidden(const Sim<P> &S) {
+#if DVC_PEND_FAST
+  return S.pend != kNoKey;
+#else
+  return S.pend != kNoKey && !((S.V >> S.pend) & 1u);
+#endif
+}
+
 // Resolve a guess at a hidden tile t (DESIGN.md §R5 APPLY), branch-free:
 // correct -> reveal t; wrong -> reveal the mover's drawn tile, or
 // its leftmost hidden tile when it drew nothing.
 template <int P, bool JOK, bool CONS>
 __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct, const KParams &kp) {
-  const bool pend_hidden = S.pend != kNoKey && !((S.V >> S.pend) & 1u);
+  const bool pend_hidden = pending_hidden(S);
   const uint32_t lmh = leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
   const uint32_t r = correct ? t : (pend_hidden ? S.pend : lmh);
   S.V |= 1u << r;
@@ -408,7 +426,7 @@ __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct,
 template <int P, bool JOK, bool CONS>
 __device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32_t t, bool correct,
                                                     const KParams &kp) {
-  const bool pend_hidden = S.pend != kNoKey && !((S.V >> S.pend) & 1u);
+  const bool pend_hidden = pending_hidden(S);
   const uint32_t lmh = leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
   const uint32_t r = correct ? t : (pend_hidden ? S.pend : lmh);
   S.V |= stop ? 0u : (1u << (r & 31u));

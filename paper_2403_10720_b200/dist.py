@@ -22,10 +22,16 @@ def shard_range(n, rank, world):
 
 
 def merge_hist(hist, group=None):
-    """a6: SUM all-reduce of the per-rank int64 winner histograms (NCCL on CUDA
-    tensors; any torch.distributed backend for the host-side tests)."""
+    """a6: SUM all-reduce of the per-rank int64 winner histograms, in place
+    (NCCL on CUDA tensors; a gloo group reduces a host copy of a CUDA tensor,
+    which lets several ranks share one GPU in the tests)."""
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+        if hist.is_cuda and dist.get_backend(group) != "nccl":
+            h = hist.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            hist.copy_(h)
+        else:
+            dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
     return hist
 
 
@@ -50,40 +56,44 @@ def rollout_batch(state, actions, n_sims, seed, node_id=0, sim_offset=0, group=N
     return rollout_batch_device(state, actions, n_sims, seed, node_id, sim_offset, group, crn=crn).cpu()
 
 
-def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, group=None):
-    """Flat root-parallel MCTS on every rank (the tree is replicated: all ranks
-    see the same all-reduced counts, so they make the same UCB1 choices and no
-    tree is ever broadcast).  Each iteration's batch of the selected child is
-    sharded over the ranks' sim ranges (DESIGN.md §R8 / §P).  Same result as
-    dvc_mcts_search on one GPU.  Returns (best_code, [(code, visits, wins)])."""
-    import math
-    codes = state.legal_actions()
-    viewer = state.info["viewer"]
-    visits = [0] * len(codes)
-    wins = [0] * len(codes)
-    N = 0
-    # root expansion: the unvisited children, in ascending code order, as one
-    # leaf-parallel batch (exactly the iterations sequential UCB1 would run)
-    k = min(expansions, len(codes))
-    order = sorted(range(len(codes)), key=lambda a: codes[a])[:k]
-    h = rollout_batch(state, [codes[a] for a in order], sims_per_child, seed, 0, 0, group)
-    for i, a in enumerate(order):
-        visits[a] = sims_per_child
-        wins[a] = int(h[i, viewer])
-        N += sims_per_child
-    for _ in range(expansions - k):
-        best, bv = None, None
-        for a in range(len(codes)):
-            if visits[a] == 0:
-                v = math.inf
+def sharded_batch(state, group=None):
+    """A batch callback for dvc.mcts_search_cb: this rank plays its contiguous
+    shard of [sim_begin, sim_end) on its GPU, then one SUM all_reduce of
+    (hist, voids) gives every rank the counts of the whole range.
+    NCCL groups reduce a CUDA tensor, others (gloo) a CPU tensor."""
+    import numpy as np
+
+    def batch(path, actions, seed, node_id, sim_begin, sim_end, flags):
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        a, b = shard_range(sim_end - sim_begin, rank, world)
+        a, b = sim_begin + a, sim_begin + b
+        P = state.players
+        hist = np.zeros((len(actions), P), dtype=np.uint64)
+        voids = np.zeros(len(actions), dtype=np.uint64)
+        if b > a:
+            if path:
+                hist, voids = dvc.rollout_path_ex(state, path, actions, seed, node_id, a, b)
             else:
-                v = wins[a] / visits[a] + c * math.sqrt(math.log(N) / visits[a])
-            if best is None or v > bv or (v == bv and codes[a] < codes[best]):
-                best, bv = a, v
-        h = rollout_batch(state, [codes[best]], sims_per_child, seed, 0, visits[best], group)
-        visits[best] += sims_per_child
-        wins[best] += int(h[0, viewer])
-        N += sims_per_child
-    stats = list(zip(codes, visits, wins))
-    best_code = min(stats, key=lambda t: (-t[1], -t[2], t[0]))[0]
-    return best_code, stats
+                hist = dvc.rollout_batch_ex(state, actions, seed, node_id, a, b, crn=bool(flags & dvc.FLAG_CRN),
+                                            informed=bool(flags & dvc.FLAG_INFORMED))
+        t = torch.from_numpy(np.concatenate([hist.reshape(-1), voids]).astype(np.int64))
+        if dist.is_initialized() and dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        merge_hist(t, group)
+        t = t.cpu().numpy().astype(np.uint64)
+        return t[:len(actions) * P].reshape(len(actions), P), (t[len(actions) * P:] if path else None)
+
+    return batch
+
+
+def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, group=None, max_depth=4, flat=1, crn=False,
+                informed=False):
+    """Root-parallel MCTS (dvc_mcts_search_cb): every rank runs the library's
+    search (UCB1 by ln_series, reading #28; flat or depth-capped tree), the
+    tree replicated on every rank; each rollout batch is sharded over the
+    ranks' sim ranges and all-reduced, so all ranks see identical counts and
+    make identical choices, and the result equals dvc_mcts_search on one GPU
+    (§R9, §P).  Returns (best_code, [(code, visits, wins)])."""
+    return dvc.mcts_search_cb(state, sharded_batch(state, group), expansions, sims_per_child, seed, c=c,
+                              max_depth=max_depth, flat=flat, crn=crn, informed=informed)

@@ -29,8 +29,9 @@ HIDDEN = 0xFF
 EXPORTS = ["dvc_state_encode", "dvc_state_query", "dvc_legal_actions", "dvc_rollout_batch",
            "dvc_rollout_batch_ex", "dvc_rollout_path_ex", "dvc_rollout_batch_async", "dvc_rollout_trace_async",
            "dvc_rollout_batch_flags_ex", "dvc_rollout_batch_flags_async", "dvc_rollout_batch_fixed_ex",
-           "dvc_sample_determinizations", "dvc_mcts_search", "dvc_md_search",
-           "dvc_set_option", "dvc_get_option", "dvc_debug_counters", "dvc_launch_count", "dvc_last_error",
+           "dvc_sample_determinizations", "dvc_mcts_search", "dvc_mcts_search_cb", "dvc_md_search",
+           "dvc_set_option", "dvc_get_option", "dvc_debug_counters", "dvc_launch_count", "dvc_transfer_bytes",
+           "dvc_last_error",
            "dvc_shutdown"]
 
 
@@ -84,6 +85,13 @@ class _StateInfo(ctypes.Structure):
                 ("n_det", ctypes.c_uint64)]
 
 
+# dvc_batch_fn (include/dvc.h): (ctx, path, path_len, actions, n_actions, seed,
+# node_id, sim_begin, sim_end, flags, hist, voids) -> status
+BATCH_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_int32,
+                            ctypes.POINTER(ctypes.c_uint32), ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint32,
+                            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
+                            ctypes.POINTER(ctypes.c_uint64))
+
 _lib = None
 
 
@@ -111,12 +119,15 @@ def lib():
         L.dvc_rollout_batch_fixed_ex.argtypes = [P(_State), P(U32), P(U64), I32, U64, U32, U64, U64, P(U64), I32]
         L.dvc_rollout_batch_flags_async.argtypes = [P(_State), P(U32), I32, U64, U32, U64, U64, U32, VP, I32, VP]
         L.dvc_mcts_search.argtypes = [P(_State), P(_SearchParams), P(_ActionStat), I32, P(I32), P(U32)]
+        L.dvc_mcts_search_cb.argtypes = [P(_State), P(_SearchParams), BATCH_FN, VP, P(_ActionStat), I32, P(I32),
+                                         P(U32)]
         L.dvc_md_search.argtypes = [P(_State), P(_MdParams), P(_ActionStat), I32, P(I32), P(U32), P(I32)]
         L.dvc_sample_determinizations.argtypes = [P(_State), U64, U32, U32, I32, P(U64)]
         L.dvc_debug_counters.argtypes = [I32, P(U32)]
         L.dvc_set_option.argtypes = [ctypes.c_char_p, I64]
         L.dvc_get_option.argtypes = [ctypes.c_char_p, P(I64)]
         L.dvc_launch_count.argtypes = [I32]
+        L.dvc_transfer_bytes.argtypes = [I32, P(U64), P(U64)]
         L.dvc_launch_count.restype = U64
         L.dvc_last_error.restype = ctypes.c_char_p
         L.dvc_shutdown.restype = None
@@ -291,11 +302,26 @@ def rollout_path_ex(state, path, actions, seed, node_id, sim_begin, sim_end, dev
     return hist, voids
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
+    """The launch stream: `stream`, else torch's current stream OF THE DEVICE
+    the output tensor lives on (not of the caller's current device)."""
     if stream is None:
         import torch
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check_out(t, shape, dtype_name, what):
+    """A device output the kernels write with atomics: CUDA, the right dtype,
+    shape and contiguous -- anything else would be written out of bounds."""
+    import torch
+    want = {"int64": torch.int64, "uint8": torch.uint8}[dtype_name]
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise ValueError("%s must be a CUDA tensor" % what)
+    if t.dtype != want or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError("%s must be a contiguous %s tensor of shape %s (got %s %s%s)"
+                         % (what, dtype_name, tuple(shape), t.dtype, tuple(t.shape),
+                            "" if t.is_contiguous() else ", non-contiguous"))
 
 
 def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist, visits=None, stream=None,
@@ -305,6 +331,11 @@ def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist,
     crn / informed: batch variants (dvc_rollout_batch_flags_async; visits
     must then be None)."""
     a, ap = _codes(actions)
+    _check_out(hist, (len(a), state.players), "int64", "hist")
+    if visits is not None:
+        _check_out(visits, (len(a),), "int64", "visits")
+        if visits.device != hist.device:
+            raise ValueError("hist and visits must be on the same device")
     dev = hist.device.index
     flags = _flags(crn, informed)
     if flags:
@@ -312,22 +343,24 @@ def rollout_batch_async(state, actions, seed, node_id, sim_begin, sim_end, hist,
             raise ValueError("the flags entry point takes no visits array")
         _check(lib().dvc_rollout_batch_flags_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin,
                                                    sim_end, flags, ctypes.c_void_p(hist.data_ptr()), dev,
-                                                   _stream_ptr(stream)))
+                                                   _stream_ptr(stream, hist.device)))
         return
     _check(lib().dvc_rollout_batch_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                          ctypes.c_void_p(hist.data_ptr()),
                                          ctypes.c_void_p(visits.data_ptr()) if visits is not None else None,
-                                         dev, _stream_ptr(stream)))
+                                         dev, _stream_ptr(stream, hist.device)))
 
 
 def rollout_trace_async(state, actions, seed, node_id, sim_begin, sim_end, hist, winners, stream=None):
     """As rollout_batch_async, plus winners[a*(sim_end-sim_begin) + s - sim_begin]
     (torch.uint8, CUDA) for every playout."""
     a, ap = _codes(actions)
+    _check_out(hist, (len(a), state.players), "int64", "hist")
+    _check_out(winners, (len(a) * (sim_end - sim_begin),), "uint8", "winners")
     dev = hist.device.index
     _check(lib().dvc_rollout_trace_async(ctypes.byref(state._s), ap, len(a), seed, node_id, sim_begin, sim_end,
                                          ctypes.c_void_p(hist.data_ptr()), ctypes.c_void_p(winners.data_ptr()),
-                                         dev, _stream_ptr(stream)))
+                                         dev, _stream_ptr(stream, hist.device)))
 
 
 def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, max_depth=4, flat=1, device=-1, crn=False,
@@ -343,6 +376,49 @@ def mcts_search(state, expansions, sims_per_child, seed, c=2 ** 0.5, max_depth=4
     tab = (_ActionStat * cap)()
     _check(lib().dvc_mcts_search(ctypes.byref(state._s), ctypes.byref(p), tab, cap, ctypes.byref(n),
                                  ctypes.byref(best)))
+    return best.value, [(t.code, t.visits, t.wins) for t in tab[:n.value]]
+
+
+def mcts_search_cb(state, batch, expansions, sims_per_child, seed, c=2 ** 0.5, max_depth=4, flat=1, crn=False,
+                   informed=False):
+    """dvc_mcts_search_cb: the library's UCT search with every rollout batch
+    delegated to batch(path, actions, seed, node_id, sim_begin, sim_end,
+    flags) -> (hist [A, P], voids [A] or None), e.g. a sharded + all-reduced
+    batch (dist.mcts_search).  Returns (best_code, [(code, visits, wins)])."""
+    P = state.players
+    err = []
+
+    def _fn(ctx, path, path_len, actions, n_actions, seed_, node_id, s0, s1, flags, hist, voids):
+        try:
+            h, v = batch([path[i] for i in range(path_len)], [actions[i] for i in range(n_actions)], seed_,
+                         node_id, s0, s1, flags)
+            h = np.asarray(h, dtype=np.uint64).reshape(-1)
+            if h.size != n_actions * P:
+                raise ValueError("batch callback returned %d counts for %d x %d" % (h.size, n_actions, P))
+            ctypes.memmove(hist, h.ctypes.data, h.nbytes)
+            if voids:
+                vv = np.zeros(n_actions, dtype=np.uint64) if v is None else np.asarray(v, dtype=np.uint64)
+                ctypes.memmove(voids, vv.ctypes.data, vv.nbytes)
+            return 0
+        except DvcError as e:
+            err.append(e)
+            return e.code
+        except Exception as e:  # surfaced below; the C side sees a failure code
+            err.append(e)
+            return -1
+
+    cb = BATCH_FN(_fn)
+    p = _SearchParams(c=c, max_depth=max_depth, expansions=expansions, sims_per_child=sims_per_child,
+                      seed=seed, flat=flat, device=-1, flags=_flags(crn, informed))
+    n = ctypes.c_int32()
+    best = ctypes.c_uint32()
+    cap = max(1, state.info["n_legal"])
+    tab = (_ActionStat * cap)()
+    rc = lib().dvc_mcts_search_cb(ctypes.byref(state._s), ctypes.byref(p), cb, None, tab, cap, ctypes.byref(n),
+                                  ctypes.byref(best))
+    if err:
+        raise err[0]
+    _check(rc)
     return best.value, [(t.code, t.visits, t.wins) for t in tab[:n.value]]
 
 
@@ -383,6 +459,14 @@ def debug_counters(device=-1):
 
 def launch_count(reset=False):
     return int(lib().dvc_launch_count(1 if reset else 0))
+
+
+def transfer_bytes(reset=False):
+    """(host->device, device->host) bytes the library moved since the last
+    reset (dvc_transfer_bytes): copies plus kernel parameter blocks."""
+    h, d = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib().dvc_transfer_bytes(1 if reset else 0, ctypes.byref(h), ctypes.byref(d)))
+    return int(h.value), int(d.value)
 
 
 def shutdown():

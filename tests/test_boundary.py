@@ -126,10 +126,8 @@ def test_options_roundtrip(dvc):
     assert dvc.get_option("block") == old and dvc.get_option("kernel") == 2   # auto
     with pytest.raises(dvc.DvcError):
         dvc.set_option("block", 1025)
-    with dvc.options(kernel=3):                            # refill2 (two playouts per lane)
-        assert dvc.get_option("kernel") == 3
     with pytest.raises(dvc.DvcError):
-        dvc.set_option("kernel", 4)
+        dvc.set_option("kernel", 3)
     with pytest.raises(dvc.DvcError):
         dvc.set_option("nope", 1)
     assert dvc.get_option("search_device") == 0            # host tree by default (north_star)

@@ -1,6 +1,6 @@
 """Small, fixed launch sequence of the bench workload, for ncu captures.
 
-    python tools/profile_run.py [--kernel refill|naive|refill2] [--sims N] [--launches L] [--workload fixtures/c2_d1.json]
+    python tools/profile_run.py [--kernel refill|naive] [--sims N] [--launches L] [--workload fixtures/c2_d1.json]
 
 Runs L rollout launches (seeds 1..L) of every legal action x N sims through the
 C-ABI on cuda:0 and prints the merged histogram checksum and the playouts per
@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--kernel", default="refill", choices=["refill", "naive", "refill2"])
+    ap.add_argument("--kernel", default="refill", choices=["refill", "naive"])
     ap.add_argument("--sims", type=int, default=1_000_000)
     ap.add_argument("--launches", type=int, default=2)
     ap.add_argument("--workload", default="fixtures/c2_d1.json")
@@ -30,7 +30,7 @@ def main():
     d = json.load(open(os.path.join(ROOT, args.workload)))
     st = dvc.encode(d)
     codes = st.legal_actions()
-    dvc.set_option("kernel", {"refill": 0, "naive": 1, "refill2": 3}[args.kernel])
+    dvc.set_option("kernel", {"refill": 0, "naive": 1}[args.kernel])
     if args.block:
         dvc.set_option("block", args.block)
     if args.grid:
