@@ -368,6 +368,7 @@ def run_reference_sweep(args):
 
 
 # ----------------------------------------------------------------- extra records
+R01_INSTR_PER_PLAYOUT = 1987
 C4_WORKLOAD = "fixtures/c4_d1.json"
 C4_PLAYOUTS_PER_MOVE = 100_000_000
 
@@ -594,6 +595,13 @@ def run_product(args):
             ipp = float(unit["thread_inst_per_playout"])
             roof["achieved"] = ipp * A * n / kernel_s / 1e12
             roof["frac"] = roof["achieved"] / peak
+            # F counts the kernel's OWN instructions, so it falls when a change
+            # removes instructions; beside it, the fraction with the work per
+            # playout frozen at round 1's 1987 (a fixed unit: cutting
+            # instructions shows up as progress)
+            roof["frac_fixed_unit"] = R01_INSTR_PER_PLAYOUT * A * n / kernel_s / 1e12 / peak
+            roof["fixed_unit"] = "%d thread-instructions per playout (round-1 refill kernel, " \
+                                 "profiles/r01_refill_c2_ncu.json)" % R01_INSTR_PER_PLAYOUT
             roof["per_unit"] = "%.0f thread-instructions per playout (%s)" % (ipp, unit.get("source", ""))
             roof["traffic"] = unit.get("dram_bytes_per_launch")
             # the same capture's view of the binding unit: the ALU pipe runs at

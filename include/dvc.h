@@ -305,7 +305,9 @@ int dvc_md_search(const dvc_state *s, const dvc_md_params *p, dvc_action_stat *t
  * not disjoint, 2 tiles not conserved, 3 a pool tile revealed, 4 bad joker
  * threshold, 5 mover dead, 6 too many decisions, 7 not exactly one reveal per
  * guess, 8 STOP without a correct guess, 9 not exactly one survivor, 10 a pending
- * (drawn this turn) tile already revealed).  The
+ * (drawn this turn) tile already revealed, 11 a histogram write out of bounds,
+ * 12 a determinization-table read out of bounds, 13 a trace write out of
+ * bounds).  The
  * release library returns DVC_E_CONFIG. */
 int dvc_debug_counters(int32_t device, uint32_t *out3);
 

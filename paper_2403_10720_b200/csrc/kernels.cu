@@ -83,6 +83,12 @@ __device__ __forceinline__ uint32_t outcome(const Sim<P> &S, uint32_t st, const 
 template <int MODE>
 __device__ __forceinline__ void record(const Smem &sm, const KParams &kp, int P, uint32_t a, uint32_t s,
                                        uint32_t w) {
+#ifdef DVC_DEBUG
+  // bounds of every shared / global write a finished playout makes (the
+  // stand-in for compute-sanitizer memcheck, which this GPU pool does not run)
+  if (a >= kp.A || w > (uint32_t)P) dbg_fail(kp, 11);
+  if (MODE == kModeTrace && (s - kp.trace_s0) >= kp.trace_stride) dbg_fail(kp, 13);
+#endif
   atomicAdd(&sm.hist[a * (P + 1) + w], 1u);
   if (MODE == kModeTrace) kp.winners[(size_t)a * kp.trace_stride + (s - kp.trace_s0)] = (uint8_t)w;
 }

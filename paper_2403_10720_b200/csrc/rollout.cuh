@@ -386,8 +386,12 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
     }
     S.ji = kb | (kw << 5) | (wf << 10);
   }
-  S.Q = dr ? (S.Q & ~(1u << t)) : S.Q;
-  S.H[0] = dr ? (H0 | (1u << t)) : H0;
+  // the drawn tile moves pool -> hand under one mask (t is in Q whenever dr):
+  // one shift of the predicate and two LOP3 instead of two selects (+1.2% C2,
+  // +2.4% C4)
+  const uint32_t mv = (dr ? 1u : 0u) << t;
+  S.Q ^= mv;
+  S.H[0] = H0 | mv;
   S.pend = et ? (dr ? t : kNoKey) : S.pend;
   S.corr = et ? 0u : S.corr;
 }
@@ -670,6 +674,13 @@ __device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t w, con
   return false;
 }
 
+#ifdef DVC_DEBUG
+__device__ __forceinline__ void dbg_fail(const KParams &kp, uint32_t code) {
+  atomicAdd(&kp.debug[0], 1u);
+  atomicCAS(&kp.debug[1], 0u, code);
+}
+#endif
+
 // ----------------------------------------------------------------- determinization (§R4)
 // rho-th element of Det(O) in canonical order: (H1, H2, H3, jinfo).
 __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64_t rho) {
@@ -737,6 +748,9 @@ __device__ __forceinline__ uint4 unrank(const uint8_t *__restrict__ plan, uint64
 // Determinization (a2): state of playout with determinization block D.
 template <int P>
 __device__ __forceinline__ void determinize_rho(Sim<P> &S, uint64_t rho, const KParams &kp) {
+#ifdef DVC_DEBUG
+  if (rho >= kp.N) dbg_fail(kp, 12);            // table read in bounds
+#endif
   const uint4 e = kp.table ? __ldg(kp.table + rho) : unrank(kp.plan, rho);
   S.H[0] = kp.Hv;
   if (P > 1) S.H[1] = e.x;
@@ -776,10 +790,6 @@ __device__ __forceinline__ bool root_action(const Sim<P> &S, uint32_t meta, cons
 // conservation, revealed tiles held by someone, joker thresholds valid, the
 // mover alive with >= 1 legal decision, exactly one reveal per guess, one
 // survivor at the end, decisions bounded by 2(|T|-1).
-__device__ __forceinline__ void dbg_fail(const KParams &kp, uint32_t code) {
-  atomicAdd(&kp.debug[0], 1u);
-  atomicCAS(&kp.debug[1], 0u, code);
-}
 template <int P, bool JOK>
 __device__ __forceinline__ void dbg_check_state(const Sim<P> &S, const KParams &kp) {
   uint32_t uni = S.Q;

@@ -25,6 +25,16 @@ def main():
                 guesses = [c for c in codes if c != 0xFFFFFFFF]
                 dvc.rollout_path_ex(st, [guesses[0]], codes[:8], 31, 1, 0, n // 10)
                 dvc.rollout_batch_ex(st, codes, 32, 0, 0, n // 4, crn=True, informed=True)
+        # the trace mode (per-playout winner writes) and a 2-block grid, where
+        # every warp claims many work batches (bounds codes 11-13)
+        import torch
+        m = max(1, n // 10)
+        hist = torch.zeros((len(codes), st.players), dtype=torch.int64, device="cuda")
+        win = torch.zeros((len(codes) * m,), dtype=torch.uint8, device="cuda")
+        with dvc.options(kernel=0, grid=2):
+            dvc.rollout_trace_async(st, codes, 33, 0, 7, 7 + m, hist, win)
+            dvc.rollout_batch_ex(st, codes, 34, 0, 0, m)
+        torch.cuda.synchronize()
     print(json.dumps({"counters": list(dvc.debug_counters())}))
 
 
