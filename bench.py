@@ -478,6 +478,8 @@ def run_product(args):
     n = args.sims
     s0, s1 = rank * n, (rank + 1) * n
     dvc.set_option("kernel", {"refill": 0, "naive": 1}[args.kernel])
+    if args.block:
+        dvc.set_option("block", args.block)
     dvc.set_option("plan_cache", 0)       # plan upload + det table rebuilt inside every step
     stream = torch.cuda.current_stream()
     hist = torch.zeros((A, P), dtype=torch.int64, device=dev)
@@ -648,6 +650,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 strong-scaling record")
+    ap.add_argument("--block", type=int, default=0, help="experiments only: refill block size (0 = default)")
     ap.add_argument("--no-deals", action="store_true", help="skip the 8-deal C2 record")
     ap.add_argument("--ref-sweep", choices=["core1", "exp1", "exp2"], default=None,
                     help="reference arm: the paper's CPU experiment sweeps (tools/paper_experiments.py)")
