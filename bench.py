@@ -367,6 +367,22 @@ def run_reference_sweep(args):
     return 0
 
 
+def all_reduce(t, op=None):
+    """SUM (or `op`) all_reduce of a CUDA tensor: NCCL directly; a gloo group
+    (BENCH_BACKEND=gloo: a functional test of the N > 1 path with several
+    ranks sharing one GPU, never a measurement) reduces a host copy."""
+    import torch
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(t, op=op)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    return t
+
+
 # ----------------------------------------------------------------- extra records
 R01_INSTR_PER_PLAYOUT = 1987
 C4_WORKLOAD = "fixtures/c4_d1.json"
@@ -403,7 +419,7 @@ def c4_strong_record(args, ws, rank, dev, stream, moves=3, warmup=1):
         if b > a:
             dvc.rollout_batch_async(st, codes, 77, 0, a, b, hist, stream=stream)
         if ws > 1:
-            torch.distributed.all_reduce(hist)
+            all_reduce(hist)
         e1.record(stream)
         torch.cuda.synchronize()
         if m >= warmup:
@@ -411,7 +427,7 @@ def c4_strong_record(args, ws, rank, dev, stream, moves=3, warmup=1):
     dvc.set_option("plan_cache", 0)
     t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
     if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t[0])
     ok = None
     if rank == 0:
@@ -463,6 +479,9 @@ def run_product(args):
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
         print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, ws), file=sys.stderr)
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if backend != "nccl":                # functional multi-rank test on one GPU
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -470,7 +489,10 @@ def run_product(args):
         # NCCL INIT logging, so the run's log shows the communicator's rank count
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     d = load_workload()
     st = dvc.encode(d)
     codes = st.legal_actions()
@@ -489,7 +511,7 @@ def run_product(args):
         hist.zero_()
         dvc.rollout_batch_async(st, codes, seed, 0, s0, s1, hist, stream=stream)
         if ws > 1:
-            torch.distributed.all_reduce(hist)
+            all_reduce(hist)
 
     for w in range(args.warmup):
         one_step(1000 + w)
@@ -515,7 +537,7 @@ def run_product(args):
             dvc.rollout_batch_async(st, codes, 1 + i, 0, s0, s1, hist, stream=stream)
             kev[i][1].record(stream)
             if ws > 1:
-                torch.distributed.all_reduce(hist)
+                all_reduce(hist)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         launches = dvc.launch_count(reset=False)
@@ -528,7 +550,7 @@ def run_product(args):
     k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
     t = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
     if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     t_ms, k_ms = float(t[0]), float(t[1])
     playouts_per_step = A * n * ws
     value = playouts_per_step * args.steps / (t_ms / 1000.0)
@@ -575,7 +597,7 @@ def run_product(args):
         for i in range(args.steps):
             h = ddist.rollout_batch(dvc.encode(d), codes, n * ws, 1 + i)   # returns host int64 [A, P]
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+        all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
         xb = dvc.transfer_bytes()
         e2e = {"value": A * n * ws * args.steps / float(dt[0]), "unit": UNIT,
                "h2d_bytes_per_step": xb[0] // args.steps, "d2h_bytes_per_step": xb[1] // args.steps + 8 * A * P,
