@@ -12,6 +12,7 @@ refill kernel.
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -85,7 +86,8 @@ def main():
                 "dram_bytes_per_launch": res["dram_bytes_per_launch"],
                 "eta_simt": res["eta_simt"], "issue_active_pct": res["issue_active_pct"],
                 "pipe_alu_pct": res.get("pipe_alu_pct"), "pipe_xu_pct": res.get("pipe_xu_pct"),
-                "pipe_fma_pct": res.get("pipe_fma_pct"), "source": out}
+                "pipe_fma_pct": res.get("pipe_fma_pct"),
+                "source": os.path.relpath(os.path.abspath(out), os.path.dirname(os.path.dirname(os.path.abspath(__file__))))}
         with open("profiles/roofline_unit.json", "w") as f:
             json.dump(unit, f, indent=1)
 
