@@ -1,7 +1,7 @@
 """GPU: the cross-GPU merge ("amalgamated")
 driven through the REAL kernels by several ranks.  A gpurun box has one GPU,
-so 2 and 3 ranks share it over gloo (dist.merge_hist reduces a host copy);
-the code path is the one torchrun + NCCL runs on 8 GPUs (shard, launch, SUM
+so 2, 3, 4 and 8 ranks (SURVEY §8(c.8) schedule invariance, G in {1,2,4,8})
+share it over gloo (dist.merge_hist reduces a host copy); the code path is the one torchrun + NCCL runs on 8 GPUs (shard, launch, SUM
 all_reduce), minus the transport.  Checked against the unsplit one-rank run
 and the oracle, including n < world (ranks with an empty shard), and the
 replicated-tree search (dist.mcts_search: the library's UCT over sharded
@@ -70,7 +70,7 @@ def dvc():
     return m
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_multi_rank_merge_on_gpu(dvc, oracle_lib, tmp_path, world):
     import torch.multiprocessing as mp
     jobs = BATCH_JOBS + SEARCH_JOBS
