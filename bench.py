@@ -486,9 +486,11 @@ def run_product(args):
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        # NCCL INIT logging, so the run's log shows the communicator's rank count
+        # NCCL INIT logging, so the run's log shows the communicator's rank
+        # count -- on stderr, so stdout keeps the one JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
