@@ -509,10 +509,10 @@ def run_product(args):
     hist = torch.zeros((A, P), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
-    def one_step(seed):
+    def one_step(seed, collective=True):
         hist.zero_()
         dvc.rollout_batch_async(st, codes, seed, 0, s0, s1, hist, stream=stream)
-        if ws > 1:
+        if ws > 1 and collective:
             all_reduce(hist)
 
     for w in range(args.warmup):
@@ -524,7 +524,10 @@ def run_product(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        clk.wait_first(load=lambda: (one_step(999), torch.cuda.synchronize()))
+        # keep the GPU busy until the sampler's first reading -- rank-local
+        # work only: each rank loops a different number of times, so a
+        # collective here would pair up wrongly across ranks and deadlock
+        clk.wait_first(load=lambda: (one_step(999, collective=False), torch.cuda.synchronize()))
         torch.cuda.synchronize()
         if ws > 1:
             torch.distributed.barrier()

@@ -42,6 +42,7 @@ struct Smem {
   uint32_t *hist, *codes, *meta, *path;
 };
 
+template <bool LUT = false>
 __device__ __forceinline__ Smem setup_smem(const KParams &kp, int P) {
   extern __shared__ uint32_t sh[];
   Smem m;
@@ -55,6 +56,9 @@ __device__ __forceinline__ Smem setup_smem(const KParams &kp, int P) {
     m.meta[i] = kp.meta[i];
   }
   if (threadIdx.x < (uint32_t)kMaxPath) m.path[threadIdx.x] = kp.path_meta[threadIdx.x];
+#if DVC_DRAW_LUT
+  if constexpr (LUT) init_nth8();
+#endif
   __syncthreads();
   return m;
 }
@@ -115,12 +119,12 @@ __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_
 }
 
 // Decision step k of a running playout (a4), given its Philox block B_k.
-template <int P, bool JOK, bool CONS, int MODE>
+template <int P, bool JOK, bool CONS, int MODE, bool LUT = false>
 __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint2 B, uint32_t k,
                                                const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                const KParams &kp, uint32_t plen) {
   constexpr bool PATH = MODE == kModePath;
-  turn_start<P, JOK>(S, st == END_TURN, B.x, kp);
+  turn_start<P, JOK, LUT>(S, st == END_TURN, B.x, kp);
 #ifdef DVC_DEBUG
   dbg_check_state<P, JOK>(S, kp);
   if (!(S.H[0] & ~S.V)) dbg_fail(kp, 5);                       // the mover is alive
@@ -167,13 +171,14 @@ template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t cb,
                                                  const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                  const KParams &kp) {
-  return step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, cb | k, kp), k, meta_of_a, path_of, a, kp, kp.path_len);
+  return step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, cb | k, kp), k, meta_of_a, path_of, a,
+                                                             kp, kp.path_len);
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
-  const Smem sm = setup_smem(kp, P);
+  const Smem sm = setup_smem<DVC_LUT_FOR(P, JOK)>(kp, P);
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kp.total; w += stride) {
     const uint32_t a = div_per(w, kp);
@@ -269,7 +274,7 @@ template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC_REFILL_MINB)
     rollout_refill_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
-  const Smem sm = setup_smem(kp, P);
+  const Smem sm = setup_smem<DVC_LUT_FOR(P, JOK)>(kp, P);
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
     // step; two flat `if (active)` blocks measured +2.8%, three steps 0%,
     // four -2%.
     if (active) {
-      st = step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+      st = step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                           kp.path_len);
       ++c1;
       if constexpr (P == 2 && !JOK) {
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
         // instead of two): +0.6% on C2; the other instantiations -0.1% (§M)
         bool fin = st == FINISH || st == VOID;
         if (!fin) {
-          st = step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+          st = step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                               kp.path_len);
           ++c1;
           fin = st == FINISH || st == VOID;
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
           active = false;
         }
         if (active) {
-          st = step_block<P, JOK, CONS, MODE>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+          st = step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                               kp.path_len);
           ++c1;
           if (st == FINISH || st == VOID) {

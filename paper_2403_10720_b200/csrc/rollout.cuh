@@ -224,6 +224,38 @@ __device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t n) {
   return 0u - nk;
 }
 
+#ifndef DVC_DRAW_LUT
+#define DVC_DRAW_LUT 1   // the draw's n-th set bit by two POPC splits + a byte table in shared memory
+#endif
+// ... used by the two-player jokerless kernels only: +0.8% on C2, but -0.6..-1.9%
+// with jokers or more players
+#define DVC_LUT_FOR(P, JOK) (DVC_DRAW_LUT != 0 && (P) == 2 && !(JOK))
+#if DVC_DRAW_LUT
+// s_nth8[y]: nibble r = position of the r-th set bit of byte y.  Filled at
+// the start of every kernel that draws through nth_bit_lut.
+__shared__ uint32_t s_nth8[256];
+__device__ __forceinline__ void init_nth8() {
+  for (uint32_t y = threadIdx.x; y < 256u; y += blockDim.x) {
+    uint32_t w = 0, r = 0;
+    for (uint32_t b = 0; b < 8u; ++b)
+      if ((y >> b) & 1u) { w |= b << (4u * r); ++r; }
+    s_nth8[y] = w;
+  }
+}
+// = nth_bit(m, n): halve by one POPC, halve again by one POPC, then the table.
+__device__ __forceinline__ uint32_t nth_bit_lut(uint32_t m, uint32_t n) {
+  const uint32_t c16 = __popc(m & 0xFFFFu);
+  const bool h = n >= c16;
+  const uint32_t w = h ? (m >> 16) : (m & 0xFFFFu);
+  const uint32_t n1 = h ? n - c16 : n;
+  const uint32_t c8 = __popc(w & 0xFFu);
+  const bool h8 = n1 >= c8;
+  const uint32_t y = (h8 ? (w >> 8) : w) & 0xFFu;
+  const uint32_t n2 = h8 ? n1 - c8 : n1;
+  return ((s_nth8[y] >> (4u * n2)) & 7u) + (h ? 16u : 0u) + (h8 ? 8u : 0u);
+}
+#endif
+
 // popc(m & below(t)) for t in [0, 31] as one clamped funnel shift (t = 0 -> 0).
 __device__ __forceinline__ uint32_t popc_below(uint32_t m, uint32_t t) {
   return (uint32_t)__popc(__funnelshift_lc(0u, m, 32u - t));
@@ -328,7 +360,7 @@ __device__ __forceinline__ uint32_t line_pos(uint32_t Hp, uint32_t v, uint32_t j
 // remainder (w * |Q|) mod 2^32, §R3).  Written
 // branch-free under the predicate `et` so lanes at different phases of a turn
 // do not diverge; the joker insertion is the only (rare) real branch.
-template <int P, bool JOK>
+template <int P, bool JOK, bool LUT = false>
 __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const KParams &kp) {
   if (P == 2) {
     const uint32_t h0 = et ? S.H[1] : S.H[0], h1 = et ? S.H[0] : S.H[1];
@@ -355,7 +387,11 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
     S.g = S.g >= (uint32_t)P ? S.g - P : S.g;
   }
   const uint64_t wq = (uint64_t)w * (uint32_t)__popc(S.Q);   // (choose, remainder) in one IMAD.WIDE
+#if DVC_DRAW_LUT
+  const uint32_t t = LUT ? nth_bit_lut(S.Q, (uint32_t)(wq >> 32)) : nth_bit(S.Q, (uint32_t)(wq >> 32));
+#else
   const uint32_t t = nth_bit(S.Q, (uint32_t)(wq >> 32));
+#endif
   const bool dr = et && S.Q != 0;
   const uint32_t H0 = S.H[0];
   if (JOK) {

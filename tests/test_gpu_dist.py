@@ -32,7 +32,8 @@ def _worker(rank, world, port, out_dir, jobs):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datetime
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=180))
     torch.cuda.set_device(0)
     from paper_2403_10720_b200 import dist as ddist, dvc
     res = {}
@@ -70,6 +71,7 @@ def dvc():
     return m
 
 
+@pytest.mark.timeout(900)
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_multi_rank_merge_on_gpu(dvc, oracle_lib, tmp_path, world):
     import torch.multiprocessing as mp
