@@ -126,7 +126,8 @@ MC_CASES = [("T1", "legal", "p_viewer", False, False), ("T1c0", "legal", "p_view
             ("T2c0", "legal", "p_viewer", False, False), ("T2c1", "legal", "p_viewer", False, False),
             ("J1", "legal", "p_viewer", False, False), ("I1", "legal", "p_viewer", False, False),
             ("I1", "legal", "p_viewer_informed", False, True), ("X3a", "p_codes", "p_all", True, False),
-            ("J2", "p_codes", "p_all", True, False), ("L1", "p_codes", "p_all", True, False),
+            ("X4a", "p_codes", "p_all", True, False), ("J2", "p_codes", "p_all", True, False),
+            ("L1", "p_codes", "p_all", True, False),
             ("E2", "legal", "p_viewer", False, False)]
 
 

@@ -1,5 +1,5 @@
-"""Writes the round-2 hand-derived goldens (tests/golden/X3a.json, J2.json,
-L1.json).  Every number below is derived by hand in the `derivation` field;
+"""Writes the round-2 hand-derived goldens (tests/golden/X3a.json, X4a.json,
+J2.json, L1.json).  Every number below is derived by hand in the `derivation` field;
 nothing here calls the oracle or the product (the tests check both against
 these values, and tests/indep_exact.py re-derives them a second way)."""
 import json, os
@@ -75,6 +75,27 @@ G = {
   "the opponent moving first: opponent guess, viewer hit, opponent guess, viewer hit -> the opponent is out first (an opponent miss only reveals its own tile). p = 1. "
   "(1,1,W1) is the same correct guess: p = 1. "
   "((1,2,B2)'s 7/10 comes from the enumerators.)")
+},
+"X4a": {
+ "citation": "PAPER:106 (the turn passes to the next gambler; a correct guess grants another attempt), PAPER:102 (last gambler standing); SPEC:186 round-robin skipping eliminated players -- here two in a row (SURVEY §8(c.7) #11)",
+ "rules": {"players": 4, "ranks": 3, "jokers": 0, "consecutive": 1},
+ "viewer": 0,
+ "lines": [[B(0, True), W(0)], [B(1, True)], [W(1, True)], [B(None), W(None)]],
+ "pool_size": 0, "pending": -1, "correct_this_turn": 0,
+ "expected": {"N": 1,
+   "legal": [[3, 0, "B", 2], [3, 1, "W", 2]],
+   "p_codes": [[3, 0, "B", 2], [3, 1, "W", 2]],
+   "p_all": [["1/2", "0", "0", "1/2"], ["1/2", "0", "0", "1/2"]]},
+ "derivation": (
+  "R=3: keys B0 W0 B1 W1 B2 W2. Seats 1 [B1] and 2 [W1] have every tile revealed: both are already eliminated. "
+  "U = T minus the viewer's {B0, W0} and the revealed {B1, W1} = {B2, W2}: seat 3's black slot is B2, its white slot W2, pool empty: N = 1. "
+  "LEGAL(0): seats 1 and 2 are skipped (dead); seat 3's black slot lists black values not held/revealed = {B2}, its white slot {W2}. "
+  "Action (3,0,B2): correct; seat 3 keeps W2, the viewer keeps W0, so two players are alive and the viewer decides again (consecutive) with "
+  "LEGAL = [(3,1,W2)] + STOP, n = 2. Guess (1/2): correct, seat 3 eliminated, the viewer wins. STOP (1/2): the next mover after seat 0 is seat 1 "
+  "-- dead -- then seat 2 -- dead -- then seat 3; no draw (pool empty); seat 3's only target is the viewer's hidden W0 slot, whose list is the white "
+  "values not in {B2, W2} and not revealed {B0, B1, W1} = {W0}: correct, the viewer is eliminated, seat 3 wins. p = (1/2, 0, 0, 1/2). "
+  "Action (3,1,W2) is the mirror image (guess B2 next, or STOP): p = (1/2, 0, 0, 1/2). "
+  "Handing the move to a dead seat instead (no skipping) would make seat 1, which has no hidden tile, move.")
 },
 }
 
