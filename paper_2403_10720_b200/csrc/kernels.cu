@@ -124,7 +124,7 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
                                                const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                const KParams &kp, uint32_t plen) {
   constexpr bool PATH = MODE == kModePath;
-  turn_start<P, JOK, LUT>(S, st == END_TURN, B.x, kp);
+  turn_start<P, JOK, LUT>(S, st == END_TURN, B.x, kp, st - 1u);   // st is DECIDE (1) or END_TURN (2) here
 #ifdef DVC_DEBUG
   dbg_check_state<P, JOK>(S, kp);
   if (!(S.H[0] & ~S.V)) dbg_fail(kp, 5);                       // the mover is alive
