@@ -356,7 +356,19 @@ void fill_kparams(KParams &kp, const State *st, uint64_t seed, uint32_t node_id,
   kp.T = st->T;
   kp.numm = (1u << (2 * st->R)) - 1u;
   kp.JB = (uint32_t)(2 * st->R);
-  kp.pend0 = st->pend_key >= 0 ? (uint32_t)st->pend_key : kNoKey;
+  // the tile a wrong root guess reveals: the viewer's pending drawn tile, or
+  // -- nothing drawn -- its leftmost hidden tile; the viewer's
+  // hidden tiles cannot change before its own wrong guess, so this is the
+  // same tile the device would find at the reveal
+  kp.pend0 = kNoKey;
+  if (st->pend_key >= 0) {
+    kp.pend0 = (uint32_t)st->pend_key;
+  } else {
+    for (int32_t i = 0; i < st->line_len[st->viewer]; ++i) {
+      const uint32_t k = st->line[st->viewer][i];
+      if (!((st->V >> k) & 1u)) { kp.pend0 = k; break; }
+    }
+  }
   kp.corr0 = (uint32_t)st->corr;
   kp.N = st->N;
   kp.debug = d->d_debug;

@@ -26,6 +26,12 @@ constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the 
 #ifndef DVC_NUMM_SKIP
 #define DVC_NUMM_SKIP 1   // jokerless kernels skip the numbered-key mask: +1.8% C2
 #endif
+#ifndef DVC_PEND_LMH
+#define DVC_PEND_LMH 1  // two-player jokerless: pend holds the leftmost hidden tile when nothing is drawn
+#endif
+#ifndef DVC_DRAW31
+#define DVC_DRAW31 1    // two-player jokerless draw without a "did it draw" predicate
+#endif
 #ifndef DVC_COLMASK
 #define DVC_COLMASK 1   // correctness test: t's colour mask by XOR, not a select
 #endif
@@ -269,7 +275,9 @@ __device__ __forceinline__ void init_nth8() {
     uint32_t w = 0, r = 0;
     for (uint32_t b = 0; b < 8u; ++b)
       if ((y >> b) & 1u) { w |= b << (4u * r); ++r; }
-    s_nth8[y] = w;
+    // byte 0 never reaches the table in a valid call; its nibble 0 is 7, so
+    // the draw from an EMPTY pool yields 24 + 7 = 31 = kNoKey (DVC_DRAW31)
+    s_nth8[y] = y ? w : 0x77777777u;
   }
 }
 // = nth_bit(m, n): halve by one POPC, halve again by one POPC, then the table.
@@ -439,7 +447,15 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
   }
   const uint64_t wq = (uint64_t)w * (uint32_t)__popc(S.Q);   // (choose, remainder) in one IMAD.WIDE
 #if DVC_DRAW_LUT
-  const uint32_t t = LUT ? nth_bit_lut(S.Q, (uint32_t)(wq >> 32)) : nth_bit(S.Q, (uint32_t)(wq >> 32));
+#if DVC_PEND_LMH
+  // an empty pool draws "the 0th set bit of the new mover's hidden tiles" =
+  // its leftmost hidden tile (no jokers: line order = key order), which is
+  // what a wrong guess of this turn reveals -- pend takes it
+  const uint32_t qsrc = (LUT && P == 2) ? (S.Q ? S.Q : (S.H[0] & ~S.V)) : S.Q;
+#else
+  const uint32_t qsrc = S.Q;
+#endif
+  const uint32_t t = LUT ? nth_bit_lut(qsrc, (uint32_t)(wq >> 32)) : nth_bit(S.Q, (uint32_t)(wq >> 32));
 #else
   const uint32_t t = nth_bit(S.Q, (uint32_t)(wq >> 32));
 #endif
@@ -473,6 +489,19 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
     }
     S.ji = kb | (kw << 5) | (wf << 10);
   }
+#if DVC_DRAW31 && DVC_ET_INT && DVC_LUT2
+  if constexpr (LUT && P == 2) {
+    // the byte-table draw returns t = kNoKey (31) for an empty pool, so no
+    // "did it draw" predicate is needed: Q holds t exactly when a tile was
+    // drawn (and never holds bit 31), and pend takes t at every turn start
+    const uint32_t mv2 = (e << t) & S.Q;
+    S.Q ^= mv2;
+    S.H[0] = H0 | mv2;
+    S.pend += e * (t - S.pend);
+    S.corr -= e * S.corr;
+    return;
+  }
+#endif
   // the drawn tile moves pool -> hand under one mask (t is in Q whenever dr):
   // one shift of the predicate and two LOP3 instead of two selects (+1.2% C2,
   // +2.4% C4)
@@ -524,9 +553,16 @@ __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct,
 template <int P, bool JOK, bool CONS>
 __device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32_t t, bool correct,
                                                     const KParams &kp) {
+#if DVC_PEND_LMH && DVC_DRAW31 && DVC_ET_INT && DVC_LUT2
+  // two players, no jokers: pend is always the tile a wrong guess reveals
+  // (the drawn tile, or the leftmost hidden one set at the turn start)
+  const uint32_t r = correct ? t : ((DVC_LUT_FOR(P, JOK)) ? S.pend
+                                   : (pending_hidden(S) ? S.pend : leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp)));
+#else
   const bool pend_hidden = pending_hidden(S);
   const uint32_t lmh = leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
   const uint32_t r = correct ? t : (pend_hidden ? S.pend : lmh);
+#endif
   S.V |= stop ? 0u : (1u << (r & 31u));
   const bool hit = correct && !stop;
   S.corr += hit ? 1u : 0u;
