@@ -42,7 +42,7 @@ struct Smem {
   uint32_t *hist, *codes, *meta, *path;
 };
 
-template <bool LUT = false>
+template <int LUT = 0>
 __device__ __forceinline__ Smem setup_smem(const KParams &kp, int P) {
   extern __shared__ uint32_t sh[];
   Smem m;
@@ -57,7 +57,7 @@ __device__ __forceinline__ Smem setup_smem(const KParams &kp, int P) {
   }
   if (threadIdx.x < (uint32_t)kMaxPath) m.path[threadIdx.x] = kp.path_meta[threadIdx.x];
 #if DVC_DRAW_LUT
-  if constexpr (LUT) init_nth8();
+  if constexpr (LUT != 0) init_nth8<LUT>();
 #endif
   __syncthreads();
   return m;
@@ -119,7 +119,7 @@ __device__ __forceinline__ uint32_t start_playout(Sim<P> &S, uint32_t s, uint32_
 }
 
 // Decision step k of a running playout (a4), given its Philox block B_k.
-template <int P, bool JOK, bool CONS, int MODE, bool LUT = false>
+template <int P, bool JOK, bool CONS, int MODE, int LUT = 0>
 __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uint2 B, uint32_t k,
                                                const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                const KParams &kp, uint32_t plen) {
@@ -163,7 +163,7 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
   return r;
 #else
   if (PATH) return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
-  return finish_decision<P, JOK, CONS>(S, stop, t, correct, kp);
+  return finish_decision<P, JOK, CONS, LUT>(S, stop, t, correct, kp);
 #endif
 }
 
@@ -171,14 +171,14 @@ template <int P, bool JOK, bool CONS, int MODE>
 __device__ __forceinline__ uint32_t step_playout(Sim<P> &S, uint32_t st, uint32_t k, uint32_t s, uint32_t cb,
                                                  const uint32_t *meta_of_a, const uint32_t *path_of, uint32_t a,
                                                  const KParams &kp) {
-  return step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, cb | k, kp), k, meta_of_a, path_of, a,
+  return step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, cb | k, kp), k, meta_of_a, path_of, a,
                                                              kp, kp.path_len);
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
-  const Smem sm = setup_smem<DVC_LUT_FOR(P, JOK)>(kp, P);
+  const Smem sm = setup_smem<DVC_LUT_KIND(P, JOK, CONS)>(kp, P);
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < kp.total; w += stride) {
     const uint32_t a = div_per(w, kp);
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
     const uint32_t cb = ctr_base(sm.codes[a], kp.node), meta = sm.meta[a];
     Sim<P> S;
     uint32_t st = start_playout<P, JOK, CONS, MODE>(S, s, cb, meta, a, kp);
-    for (uint32_t k = 0; st != FINISH && st != VOID; ++k)
+    for (uint32_t k = 0; st != FINISH && !(PATH && st == VOID); ++k)
       st = step_playout<P, JOK, CONS, MODE>(S, st, k, s, cb, sm.meta, sm.path, a, kp);
     record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
   }
@@ -274,7 +274,7 @@ template <int P, bool JOK, bool CONS, int MODE>
 __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC_REFILL_MINB)
     rollout_refill_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
-  const Smem sm = setup_smem<DVC_LUT_FOR(P, JOK)>(kp, P);
+  const Smem sm = setup_smem<DVC_LUT_KIND(P, JOK, CONS)>(kp, P);
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -348,34 +348,34 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
     // step; two flat `if (active)` blocks measured +2.8%, three steps 0%,
     // four -2%.
     if (active) {
-      st = step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+      st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                           kp.path_len);
       ++c1;
       if constexpr (P == 2 && !JOK) {
         // one record site per iteration: a lane that finishes in the first
         // step skips the second and records after it (one divergent region
         // instead of two): +0.6% on C2; the other instantiations -0.1% (§M)
-        bool fin = st == FINISH || st == VOID;
+        bool fin = st == FINISH || (PATH && st == VOID);   // VOID exists in path batches only
         if (!fin) {
-          st = step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+          st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                               kp.path_len);
           ++c1;
-          fin = st == FINISH || st == VOID;
+          fin = st == FINISH || (PATH && st == VOID);
         }
         if (fin) {
           record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
           active = false;
         }
       } else {
-        if (st == FINISH || st == VOID) {
+        if (st == FINISH || (PATH && st == VOID)) {
           record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
           active = false;
         }
         if (active) {
-          st = step_block<P, JOK, CONS, MODE, DVC_LUT_FOR(P, JOK)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+          st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                               kp.path_len);
           ++c1;
-          if (st == FINISH || st == VOID) {
+          if (st == FINISH || (PATH && st == VOID)) {
             record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
             active = false;
           }

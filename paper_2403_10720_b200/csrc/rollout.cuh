@@ -26,6 +26,9 @@ constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the 
 #ifndef DVC_NUMM_SKIP
 #define DVC_NUMM_SKIP 1   // jokerless kernels skip the numbered-key mask: +1.8% C2
 #endif
+#ifndef DVC_LUT3
+#define DVC_LUT3 1      // byte-table draw with IMAD-shifted counts and a byte-per-entry table
+#endif
 #ifndef DVC_PEND_LMH
 #define DVC_PEND_LMH 1  // two-player jokerless: pend holds the leftmost hidden tile when nothing is drawn
 #endif
@@ -34,9 +37,6 @@ constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the 
 #endif
 #ifndef DVC_COLMASK
 #define DVC_COLMASK 1   // correctness test: t's colour mask by XOR, not a select
-#endif
-#ifndef DVC_LUT2
-#define DVC_LUT2 1      // byte-table draw with the offset as a shift amount
 #endif
 #ifndef DVC_REM_TRACK
 #define DVC_REM_TRACK 1   // the weighted probes carry x - (weight below) instead of the weight
@@ -266,42 +266,63 @@ __device__ __forceinline__ uint32_t nth_bit(uint32_t m, uint32_t n) {
 // ... used by the two-player jokerless kernels only: +0.8% on C2, but -0.6..-1.9%
 // with jokers or more players
 #define DVC_LUT_FOR(P, JOK) (DVC_DRAW_LUT != 0 && (P) == 2 && !(JOK))
+// which table: the byte-per-entry one under consecutive rules (+0.6% C2), the
+// nibble one otherwise (the byte table measured -2.2% with consecutive = 0)
+#define DVC_LUT_KIND(P, JOK, CONS) (DVC_LUT_FOR(P, JOK) ? ((DVC_LUT3 && (CONS)) ? 3 : 2) : 0)
 #if DVC_DRAW_LUT
-// s_nth8[y]: nibble r = position of the r-th set bit of byte y.  Filled at
-// the start of every kernel that draws through nth_bit_lut.
+// Draw tables.  s_nth8[y]: nibble r = the r-th set bit of byte y (kind 2);
+// s_nth8b[8 y + r]: the same, one byte per entry (kind 3).  Byte 0 never
+// reaches a table in a valid call; its entries say 7, so a draw from an EMPTY
+// mask yields 24 + 7 = 31 = kNoKey.  Filled at the start of every kernel that
+// draws through nth_bit_lut.
 __shared__ uint32_t s_nth8[256];
+__shared__ uint8_t s_nth8b[2048];
+template <int KIND>
 __device__ __forceinline__ void init_nth8() {
-  for (uint32_t y = threadIdx.x; y < 256u; y += blockDim.x) {
-    uint32_t w = 0, r = 0;
-    for (uint32_t b = 0; b < 8u; ++b)
-      if ((y >> b) & 1u) { w |= b << (4u * r); ++r; }
-    // byte 0 never reaches the table in a valid call; its nibble 0 is 7, so
-    // the draw from an EMPTY pool yields 24 + 7 = 31 = kNoKey (DVC_DRAW31)
-    s_nth8[y] = y ? w : 0x77777777u;
+  if constexpr (KIND == 3) {
+    for (uint32_t i = threadIdx.x; i < 2048u; i += blockDim.x) {
+      const uint32_t y = i >> 3, r = i & 7u;
+      uint32_t c = 0, pos = 7;
+      for (uint32_t b = 0; b < 8u; ++b)
+        if ((y >> b) & 1u) { if (c == r) { pos = b; break; } ++c; }
+      s_nth8b[i] = (uint8_t)(y ? pos : 7u);
+    }
+  } else {
+    for (uint32_t y = threadIdx.x; y < 256u; y += blockDim.x) {
+      uint32_t w = 0, r = 0;
+      for (uint32_t b = 0; b < 8u; ++b)
+        if ((y >> b) & 1u) { w |= b << (4u * r); ++r; }
+      s_nth8[y] = y ? w : 0x77777777u;
+    }
   }
 }
-// = nth_bit(m, n): halve by one POPC, halve again by one POPC, then the table.
+// = nth_bit(m, n): halve by one POPC, halve again by one POPC, then a table;
+// the byte offset is the shift amount and the result is the table entry + it.
+template <int KIND>
 __device__ __forceinline__ uint32_t nth_bit_lut(uint32_t m, uint32_t n) {
-  const uint32_t c16 = __popc(m & 0xFFFFu);
-  const bool h = n >= c16;
-#if DVC_LUT2
-  // the byte's offset as a shift amount: the result is the table nibble + sh
-  uint32_t sh = h ? 16u : 0u;
-  const uint32_t n1 = h ? n - c16 : n;
-  const uint32_t c8 = __popc((m >> sh) & 0xFFu);
-  const bool h8 = n1 >= c8;
-  sh += h8 ? 8u : 0u;
-  const uint32_t n2 = h8 ? n1 - c8 : n1;
-  return ((s_nth8[(m >> sh) & 0xFFu] >> (4u * n2)) & 7u) + sh;
-#else
-  const uint32_t w = h ? (m >> 16) : (m & 0xFFFFu);
-  const uint32_t n1 = h ? n - c16 : n;
-  const uint32_t c8 = __popc(w & 0xFFu);
-  const bool h8 = n1 >= c8;
-  const uint32_t y = (h8 ? (w >> 8) : w) & 0xFFu;
-  const uint32_t n2 = h8 ? n1 - c8 : n1;
-  return ((s_nth8[y] >> (4u * n2)) & 7u) + (h ? 16u : 0u) + (h8 ? 8u : 0u);
-#endif
+  if constexpr (KIND == 3) {
+    // low-part counts by multiplies (popc(m << 16), popc(byte << 24): IMADs
+    // instead of masks) and a byte per entry (no nibble extraction)
+    const uint32_t c16 = __popc(m << 16);
+    const bool h = n >= c16;
+    uint32_t sh = h ? 16u : 0u;
+    const uint32_t n1 = h ? n - c16 : n;
+    const uint32_t c8 = __popc((m >> sh) << 24);
+    const bool h8 = n1 >= c8;
+    sh += h8 ? 8u : 0u;
+    const uint32_t n2 = h8 ? n1 - c8 : n1;
+    return (uint32_t)s_nth8b[((m >> sh) & 0xFFu) * 8u + n2] + sh;
+  } else {
+    const uint32_t c16 = __popc(m & 0xFFFFu);
+    const bool h = n >= c16;
+    uint32_t sh = h ? 16u : 0u;
+    const uint32_t n1 = h ? n - c16 : n;
+    const uint32_t c8 = __popc((m >> sh) & 0xFFu);
+    const bool h8 = n1 >= c8;
+    sh += h8 ? 8u : 0u;
+    const uint32_t n2 = h8 ? n1 - c8 : n1;
+    return ((s_nth8[(m >> sh) & 0xFFu] >> (4u * n2)) & 7u) + sh;
+  }
 }
 #endif
 
@@ -409,7 +430,7 @@ __device__ __forceinline__ uint32_t line_pos(uint32_t Hp, uint32_t v, uint32_t j
 // remainder (w * |Q|) mod 2^32, §R3).  Written
 // branch-free under the predicate `et` so lanes at different phases of a turn
 // do not diverge; the joker insertion is the only (rare) real branch.
-template <int P, bool JOK, bool LUT = false>
+template <int P, bool JOK, int LUT = 0>
 __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const KParams &kp, uint32_t e = 0u) {
   // e: et as 0/1 (the step state minus one), so the two-player turn start
   // swaps and resets by IMADs instead of selects (DVC_ET_INT: +0.5% C2, +1.1%
@@ -451,11 +472,13 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
   // an empty pool draws "the 0th set bit of the new mover's hidden tiles" =
   // its leftmost hidden tile (no jokers: line order = key order), which is
   // what a wrong guess of this turn reveals -- pend takes it
-  const uint32_t qsrc = (LUT && P == 2) ? (S.Q ? S.Q : (S.H[0] & ~S.V)) : S.Q;
+  const uint32_t qsrc = (LUT != 0 && P == 2) ? (S.Q ? S.Q : (S.H[0] & ~S.V)) : S.Q;
 #else
   const uint32_t qsrc = S.Q;
 #endif
-  const uint32_t t = LUT ? nth_bit_lut(qsrc, (uint32_t)(wq >> 32)) : nth_bit(S.Q, (uint32_t)(wq >> 32));
+  uint32_t t;
+  if constexpr (LUT != 0) t = nth_bit_lut<LUT>(qsrc, (uint32_t)(wq >> 32));
+  else t = nth_bit(S.Q, (uint32_t)(wq >> 32));
 #else
   const uint32_t t = nth_bit(S.Q, (uint32_t)(wq >> 32));
 #endif
@@ -489,8 +512,8 @@ __device__ __forceinline__ void turn_start(Sim<P> &S, bool et, uint32_t w, const
     }
     S.ji = kb | (kw << 5) | (wf << 10);
   }
-#if DVC_DRAW31 && DVC_ET_INT && DVC_LUT2
-  if constexpr (LUT && P == 2) {
+#if DVC_DRAW31 && DVC_ET_INT
+  if constexpr (LUT != 0 && P == 2) {
     // the byte-table draw returns t = kNoKey (31) for an empty pool, so no
     // "did it draw" predicate is needed: Q holds t exactly when a tile was
     // drawn (and never holds bit 31), and pend takes t at every turn start
@@ -550,13 +573,14 @@ __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct,
 // The end of a decision step without a branch on STOP: a STOP (stop = true)
 // reveals nothing and ends the turn, any guess resolves as above.  Lanes that
 // stop and lanes that guess run the same instructions (no divergent region).
-template <int P, bool JOK, bool CONS>
+template <int P, bool JOK, bool CONS, int LUT = 0>
 __device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32_t t, bool correct,
                                                     const KParams &kp) {
-#if DVC_PEND_LMH && DVC_DRAW31 && DVC_ET_INT && DVC_LUT2
+#if DVC_PEND_LMH && DVC_DRAW31 && DVC_ET_INT
   // two players, no jokers: pend is always the tile a wrong guess reveals
   // (the drawn tile, or the leftmost hidden one set at the turn start)
-  const uint32_t r = correct ? t : ((DVC_LUT_FOR(P, JOK)) ? S.pend
+  // (only in kernels whose turn start draws through the table: LUT != 0)
+  const uint32_t r = correct ? t : ((LUT != 0 && P == 2) ? S.pend
                                    : (pending_hidden(S) ? S.pend : leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp)));
 #else
   const bool pend_hidden = pending_hidden(S);
