@@ -26,6 +26,12 @@ constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the 
 #ifndef DVC_NUMM_SKIP
 #define DVC_NUMM_SKIP 1   // jokerless kernels skip the numbered-key mask: +1.8% C2
 #endif
+#ifndef DVC_FIN_OWNER
+#define DVC_FIN_OWNER 1   // table-draw kernels: game over tested on the revealed tile's owner only
+#endif
+#ifndef DVC_NW_ALL
+#define DVC_NW_ALL 1      // nW = popc(avail) - nB: no white-mask LOP3
+#endif
 #ifndef DVC_LUT3
 #define DVC_LUT3 1      // byte-table draw with IMAD-shifted counts and a byte-per-entry table
 #endif
@@ -591,11 +597,18 @@ __device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32
     const uint32_t lmh = leftmost_hidden<JOK>(S.H[0], S.V, S.ji, kp);
     r = correct ? t : (pend_hidden ? S.pend : lmh);
   }
+  constexpr bool kTab2 = DVC_PEND_LMH && DVC_DRAW31 && DVC_ET_INT && LUT != 0 && P == 2;
   S.V |= stop ? 0u : (1u << (r & 31u));
   const bool hit = correct && !stop;
   S.corr += hit ? 1u : 0u;
   const uint32_t cont = (CONS && hit) ? DECIDE : END_TURN;
-  return (!stop && over(S)) ? FINISH : cont;
+  if constexpr (kTab2 && DVC_FIN_OWNER) {
+    // two players: only the owner of the revealed tile can have run out --
+    // the opponent after a correct guess, the mover after a wrong one
+    return (!stop && !((correct ? S.H[1] : S.H[0]) & ~S.V)) ? FINISH : cont;
+  } else {
+    return (!stop && over(S)) ? FINISH : cont;
+  }
 }
 
 // Hidden tile of opponent hand Hd selected by index x of the mover's LEGAL
@@ -671,8 +684,13 @@ template <int P, bool JOK, bool CONS>
 __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t w, const KParams &kp, uint32_t *t_out,
                                        bool *correct) {
   const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
-  const uint32_t aB = avail & kEven, aW = avail & kOdd;
+  const uint32_t aB = avail & kEven;
+#if DVC_NW_ALL
+  const uint32_t nB = __popc(aB), nW = __popc(avail) - nB;   // no white mask: one LOP3 fewer, an IADD more
+#else
+  const uint32_t aW = avail & kOdd;
   const uint32_t nB = __popc(aB), nW = __popc(aW);
+#endif
   uint32_t cnt[P];
   uint32_t tot = 0;
 #pragma unroll
@@ -707,7 +725,7 @@ __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t w, const KParam
   // 0 - (t & 1) (an IMAD), one 3-input LOP3 with avail -- no select
   *correct = vidx == popc_below(avail & (kEven ^ (0u - (t & 1u))), t);
 #else
-  *correct = vidx == popc_below((t & 1u) ? aW : aB, t);
+  *correct = vidx == popc_below((t & 1u) ? (avail & kOdd) : aB, t);
 #endif
   return stop;
 }
