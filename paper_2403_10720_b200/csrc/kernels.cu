@@ -135,6 +135,7 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
   uint32_t t;
   bool correct;
   bool stop;
+  uint32_t hd = 0u;   // the target's hand (3-4 players: the live-seat count, DVC_ALIVE_CNT)
   if (PATH && S.fi <= plen && S.g == kp.g0) {
     // deep-tree batch: the viewer's next forced action F[fi] (the batch
     // action itself at fi == path_len) replaces the random decision
@@ -144,9 +145,9 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
     S.fi += 1;
     if (illegal) return VOID;
   } else if constexpr (MODE == kModeInformed) {
-    stop = decide_informed<P, JOK, CONS>(S, B.y, kp, &t, &correct);
+    stop = decide_informed<P, JOK, CONS>(S, B.y, kp, &t, &correct, &hd);
   } else {
-    stop = decide<P, JOK, CONS>(S, B.y, kp, &t, &correct);
+    stop = decide<P, JOK, CONS>(S, B.y, kp, &t, &correct, &hd);
   }
 #ifdef DVC_DEBUG
   const uint32_t r = stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
@@ -163,7 +164,7 @@ __device__ __forceinline__ uint32_t step_block(Sim<P> &S, uint32_t st, const uin
   return r;
 #else
   if (PATH) return stop ? END_TURN : resolve<P, JOK, CONS>(S, t, correct, kp);
-  return finish_decision<P, JOK, CONS, LUT>(S, stop, t, correct, kp);
+  return finish_decision<P, JOK, CONS, LUT>(S, stop, t, correct, kp, hd);
 #endif
 }
 
@@ -205,17 +206,19 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
 // retire via __ballot_sync and pull new playouts from a work counter).
 constexpr uint32_t kRing = kRingSlots;
 
-template <int P>
+template <int P, bool JOK, bool CONS>
 struct RingView {
   // AoS, ring_vecs(P) x 16 B per slot: a pop is 3-4 LDS.128 -- pops run in a
   // divergent region with ~2 lanes, so instructions, not bank conflicts, are
   // what they cost.  Words: H[P], V, Q, ji, g, pend, corr, st | fi << 4, a, s
   // and the playout's Philox counter word c1 for step 0 (ctr_base(code,
-  // node), §R3).  The turn fields are unpacked -- no shifts and masks on a pop;
+  // node), §R3), then the live-seat count na for 3-4 players.  The turn
+  // fields are unpacked -- no shifts and masks on a pop;
   // packing them into one word (one vector less for 3-4 players) measured
   // 3.6% (2p), 1.4% (3p) and 1.0% (4p) slower.
-  static constexpr int kNW = P + 10;   // words used
+  static constexpr int kNW = P + 10 + (kAliveSlot(P) ? 1 : 0);   // words used
   static constexpr uint32_t V = (kNW + 3) / 4;
+  static_assert(V == ring_vecs(P), "ring slot size (host smem sizing) out of step");
   uint4 *base;
   template <bool PATH>
   __device__ __forceinline__ void put(uint32_t i, const Sim<P> &S, uint32_t st, uint32_t a, uint32_t s,
@@ -233,6 +236,7 @@ struct RingView {
     w[P + 7] = a;
     w[P + 8] = s;
     w[P + 9] = c1;
+    if constexpr (kAliveSlot(P)) w[P + 10] = kAliveCnt<P, JOK, CONS> ? S.na : 0u;
 #pragma unroll
     for (int q = kNW; q < 16; ++q) w[q] = 0;
     uint4 *b = base + V * i;
@@ -262,6 +266,7 @@ struct RingView {
     a = w[P + 7];
     s = w[P + 8];
     c1 = w[P + 9];
+    if constexpr (kAliveCnt<P, JOK, CONS>) S.na = w[P + 10];
   }
 };
 
@@ -278,7 +283,8 @@ __global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC
   extern __shared__ uint32_t sh_all[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const RingView<P> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) + (threadIdx.x >> 5) * RingView<P>::V * kRing};
+  const RingView<P, JOK, CONS> ring{reinterpret_cast<uint4 *>(sh_all + ring_word_offset(kp.A, P)) +
+                             (threadIdx.x >> 5) * RingView<P, JOK, CONS>::V * kRing};
   // Warp-uniform work batch: sims s0 + [cs, ce) of action ca (kBatch-aligned
   // slices of ONE action, so no per-lane division).  The next batch index is
   // claimed one batch ahead (lane 0's atomicAdd result is only read at the

@@ -53,13 +53,19 @@ constexpr uint32_t kBatch = DVC_KBATCH;   // sims per work-counter claim of the 
 #ifndef DVC_ET_INT
 #define DVC_ET_INT 1   // two-player turn start driven by the step state as an integer
 #endif
+#ifndef DVC_ALIVE_CNT
+#define DVC_ALIVE_CNT 1   // 3-4 players: the state counts its live seats; game over from the revealed tile's owner
+#endif
 constexpr uint32_t kRingSlots = 64;                          // started playouts per warp
 // 16 B vectors per refill-kernel ring slot (kernels.cu RingView): P + 10 words
-// (unpacked turn fields).  (Carrying the
+// (unpacked turn fields), + 1 for the live-seat count of 3-4 players (fits the
+// same 4 vectors).  (Carrying the
 // next step's Philox block instead, so it could be generated during the
 // current step, measured -7% with Philox4x32 and -0.5..+1% with Philox2x32:
 // not kept.)
-__host__ __device__ constexpr uint32_t ring_vecs(int P) { return (uint32_t)(P + 10 + 3) / 4u; }
+__host__ __device__ constexpr uint32_t ring_vecs(int P) {
+  return (uint32_t)(P + 10 + ((DVC_ALIVE_CNT != 0 && P > 2) ? 1 : 0) + 3) / 4u;   // kAliveSlot
+}
 
 constexpr uint32_t FINISH = 0, DECIDE = 1, END_TURN = 2, VOID = 3;
 constexpr uint32_t kCrnWord = 0xFFFFFFFEu;   // D's code under common random numbers (no action code, §R3)
@@ -355,7 +361,25 @@ struct Sim {
   uint32_t pend;   // key drawn this turn or kNoKey
   uint32_t corr;   // correct guesses this turn
   uint32_t fi;     // deep-tree batches: forced viewer actions applied so far
+  uint32_t na;     // 3-4 players (DVC_ALIVE_CNT): seats with a hidden tile
 };
+
+// the live-seat count has a ring slot word (P + 10) for 3-4 players, and
+// ends the game in the kernels where it measured faster: 3 players with
+// jokers (+1.1%, consecutive = 0 +0.7%), 3 players jokerless consecutive
+// (+1.5%), 4 players jokerless (+2.6%, +2.9%) -- not 4 players with jokers
+// (C4 -1.5%) nor 3 players jokerless consecutive = 0 (-0.7%)
+__host__ __device__ constexpr bool kAliveSlot(int P) { return DVC_ALIVE_CNT != 0 && P > 2; }
+template <int P, bool JOK, bool CONS>
+constexpr bool kAliveCnt = kAliveSlot(P) && !(P == 4 && JOK) && !(P == 3 && !JOK && !CONS);
+
+template <int P>
+__device__ __forceinline__ uint32_t alive_seats(const Sim<P> &S) {
+  uint32_t alive = 0;
+#pragma unroll
+  for (int d = 0; d < P; ++d) alive += (S.H[d] & ~S.V) ? 1u : 0u;
+  return alive;
+}
 
 template <int P>
 __device__ __forceinline__ bool over(const Sim<P> &S) {
@@ -573,7 +597,12 @@ __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct,
   S.V |= 1u << r;
   S.corr += correct ? 1u : 0u;
   const uint32_t cont = (CONS && correct) ? DECIDE : END_TURN;   // PAPER:106 vs PAPER:153
-  return over(S) ? FINISH : cont;
+  if constexpr (kAliveCnt<P, JOK, CONS>) {
+    S.na = alive_seats(S);
+    return S.na <= 1u ? FINISH : cont;
+  } else {
+    return over(S) ? FINISH : cont;
+  }
 }
 
 // The end of a decision step without a branch on STOP: a STOP (stop = true)
@@ -581,7 +610,7 @@ __device__ __forceinline__ uint32_t resolve(Sim<P> &S, uint32_t t, bool correct,
 // stop and lanes that guess run the same instructions (no divergent region).
 template <int P, bool JOK, bool CONS, int LUT = 0>
 __device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32_t t, bool correct,
-                                                    const KParams &kp) {
+                                                    const KParams &kp, uint32_t hd = 0u) {
   uint32_t r;
   if constexpr (DVC_PEND_LMH && DVC_DRAW31 && DVC_ET_INT && LUT != 0 && P == 2) {
     // two players, no jokers, table draw: pend is always the tile a wrong
@@ -606,6 +635,12 @@ __device__ __forceinline__ uint32_t finish_decision(Sim<P> &S, bool stop, uint32
     // two players: only the owner of the revealed tile can have run out --
     // the opponent after a correct guess, the mover after a wrong one
     return (!stop && !((correct ? S.H[1] : S.H[0]) & ~S.V)) ? FINISH : cont;
+  } else if constexpr (kAliveCnt<P, JOK, CONS>) {
+    // 3-4 players: only the revealed tile's owner (the target hd after a
+    // correct guess, the mover after a wrong one) can have run out; the game
+    // is over when one live seat is left
+    S.na -= (!stop && !((correct ? hd : S.H[0]) & ~S.V)) ? 1u : 0u;
+    return S.na <= 1u ? FINISH : cont;
   } else {
     return (!stop && over(S)) ? FINISH : cont;
   }
@@ -682,7 +717,7 @@ __device__ __forceinline__ void select_slot(uint32_t Hd, uint32_t V, uint32_t ji
 // equals t exactly when vidx = #available values of that colour below t.
 template <int P, bool JOK, bool CONS>
 __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t w, const KParams &kp, uint32_t *t_out,
-                                       bool *correct) {
+                                       bool *correct, uint32_t *hd_out = nullptr) {
   const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
   const uint32_t aB = avail & kEven;
 #if DVC_NW_ALL
@@ -720,6 +755,7 @@ __device__ __forceinline__ bool decide(const Sim<P> &S, uint32_t w, const KParam
   uint32_t t, vidx;
   select_slot<JOK, DVC_REM_FOR(P, JOK)>(Hd, S.V, S.ji, nB, nW, x, kp, &t, &vidx);
   *t_out = t;
+  if (hd_out) *hd_out = Hd;
 #if DVC_COLMASK
   // the available values of t's colour: kEven flipped to kOdd by XOR with
   // 0 - (t & 1) (an IMAD), one 3-input LOP3 with avail -- no select
@@ -827,7 +863,7 @@ __device__ __forceinline__ void informed_select(const InfCtx &c, uint32_t Hd, ui
 // One informed decision: as decide(), over the order-aware list.
 template <int P, bool JOK, bool CONS>
 __device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t w, const KParams &kp, uint32_t *t_out,
-                                                bool *correct) {
+                                                bool *correct, uint32_t *hd_out = nullptr) {
   const uint32_t avail = kp.T & ~S.H[0] & ~S.V;
   InfCtx c;
   c.num[0] = avail & kp.numm & kEven;
@@ -856,6 +892,7 @@ __device__ __forceinline__ bool decide_informed(const Sim<P> &S, uint32_t w, con
     }
     x -= sub;
   }
+  if (hd_out) *hd_out = Hd;
   if (stop) {
     *t_out = kNoKey;
     *correct = false;
@@ -960,6 +997,7 @@ __device__ __forceinline__ void determinize_rho(Sim<P> &S, uint64_t rho, const K
   S.g = kp.g0;
   S.pend = kp.pend0;
   S.corr = kp.corr0;
+  if constexpr (kAliveSlot(P)) S.na = alive_seats(S);   // dead code where unused
 }
 
 template <int P>
