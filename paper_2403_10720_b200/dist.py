@@ -48,6 +48,10 @@ def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, 
     if s1 > s0:
         dvc.rollout_batch_async(state, actions, seed, node_id, sim_offset + s0, sim_offset + s1, hist,
                                 stream=stream, crn=crn)
+    if stream is not None:
+        # the all_reduce (and a gloo host copy) run on torch's current stream:
+        # order them after the kernel on the caller's stream
+        torch.cuda.current_stream(dev).wait_stream(stream)
     return merge_hist(hist, group)
 
 

@@ -44,6 +44,13 @@ def _worker(rank, world, port, out_dir, jobs):
             n, seed, off = args
             h = ddist.rollout_batch(st, st.legal_actions(), n, seed, 0, off)
             res[key] = h.tolist()
+        elif kind == "batch_stream":
+            # launched on a side stream: the merge (on the current stream)
+            # must be ordered after the kernel
+            n, seed, off = args
+            side = torch.cuda.Stream()
+            h = ddist.rollout_batch_device(st, st.legal_actions(), n, seed, 0, off, stream=side)
+            res[key] = h.cpu().tolist()
         else:
             exp_n, n, seed, flat = args
             best, stats = ddist.mcts_search(st, exp_n, n, seed, flat=flat)
@@ -57,7 +64,8 @@ def _worker(rank, world, port, out_dir, jobs):
 BATCH_JOBS = [("c2_300", "batch", "fixtures/c2_d1.json", (300001, 7, 0)),
               ("c4_small", "batch", "fixtures/c4_d2.json", (2, 3, 0)),        # n < world for world 3
               ("x3_off", "batch", "fixtures/x3_d1.json", (5000, 9, 1 << 20)),
-              ("c3_j", "batch", "fixtures/c3_d2.json", (20011, 5, 0))]
+              ("c3_j", "batch", "fixtures/c3_d2.json", (20011, 5, 0)),
+              ("c2_side", "batch_stream", "fixtures/c2_d1.json", (1000003, 8, 0))]
 SEARCH_JOBS = [("s_flat", "search", "fixtures/c3_d1.json", (96, 257, 21, 1)),
                ("s_deep", "search", "fixtures/c2_d2.json", (40, 129, 5, 0)),
                ("s_x3", "search", "fixtures/x3_d1.json", (60, 65, 2, 1))]
@@ -84,14 +92,14 @@ def test_multi_rank_merge_on_gpu(dvc, oracle_lib, tmp_path, world):
         st = dvc.encode(d)
         for r in range(1, world):
             assert ranks[r][key] == ranks[0][key], (key, r)       # every rank holds the merged result
-        if kind == "batch":
+        if kind in ("batch", "batch_stream"):
             n, seed, off = args
             codes = st.legal_actions()
             one = dvc.rollout_batch_ex(st, codes, seed, 0, off, off + n).tolist()
             assert ranks[0][key] == one, key                      # == the unsplit single-rank run
             if n <= 5000:
                 assert ranks[0][key] == oracle_lib.rollout(d, codes, seed, 0, off, off + n), key
-            else:                                                 # oracle on a strided sample of rows
+            elif n <= 400000:                                     # oracle on a strided sample of rows
                 for a in range(0, len(codes), 7):
                     sub = oracle_lib.rollout(d, [codes[a]], seed, 0, off, off + n)[0]
                     assert ranks[0][key][a] == sub, (key, a)
