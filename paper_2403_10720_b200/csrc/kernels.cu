@@ -22,18 +22,33 @@
 
 namespace dvc {
 
-// Register cap of the refill kernel as min resident 256-thread blocks per SM.
-// Two players without jokers: 4 (64 registers; 8 blocks of 128 per SM), +1.3%
-// on C2; with jokers or more players the cap costs more than the occupancy
-// gains (C3 -3%, C4 -2.4%), so 3.  Tighter caps for two players (56 or 52
-// registers, 9-10 blocks) measured -3% / -4%.
+// Register cap of the refill kernel as min resident 256-thread blocks per SM,
+// per instantiation (resident 128-thread blocks then follow from the
+// registers used; the grid is sized from the occupancy API).  Two players
+// without jokers: 4 (64 registers; 8 blocks of 128 per SM), +1.3% on C2
+// (56 or 52 registers, 9-10 blocks: -3% / -4%).  Round 2 sweep of 2 / 3 / 4
+// (DESIGN.md §M): two players with jokers 2 (80 registers, +2.3% C3 over 3,
+// consecutive = 0 +2.6%), three players jokerless consecutive 4 (64
+// registers, +1.4%; consecutive = 0 -1.1%), four players jokerless
+// consecutive = 0 2 (+0.6%; consecutive -3.1%); otherwise 3 (C4 -0.1% /
+// -0.4% at 4 / 2).
 #ifndef DVC_REFILL_MINB2
 #define DVC_REFILL_MINB2 4
 #endif
 #ifndef DVC_REFILL_MINB
 #define DVC_REFILL_MINB 3
 #endif
-
+#ifndef DVC_MINB_PER_INST
+#define DVC_MINB_PER_INST 1
+#endif
+constexpr int refill_minb(int P, bool JOK, bool CONS) {
+  if (P == 2 && !JOK) return DVC_REFILL_MINB2;
+  if (!DVC_MINB_PER_INST) return DVC_REFILL_MINB;
+  if (P == 2) return 2;
+  if (P == 3 && !JOK && CONS) return 4;
+  if (P == 4 && !JOK && !CONS) return 2;
+  return DVC_REFILL_MINB;
+}
 
 // Shared memory: hist[A*P] u32 counters, then the action codes and metas
 // (read once per playout start; per-lane indexed, so smem beats the param bank).
@@ -276,7 +291,7 @@ __host__ __device__ __forceinline__ uint32_t ring_word_offset(uint32_t A, int P)
 }
 
 template <int P, bool JOK, bool CONS, int MODE>
-__global__ void __launch_bounds__(256, (P == 2 && !JOK) ? DVC_REFILL_MINB2 : DVC_REFILL_MINB)
+__global__ void __launch_bounds__(256, refill_minb(P, JOK, CONS))
     rollout_refill_kernel(const __grid_constant__ KParams kp) {
   constexpr bool PATH = MODE == kModePath;
   const Smem sm = setup_smem<DVC_LUT_KIND(P, JOK, CONS)>(kp, P);

@@ -45,13 +45,16 @@ def rollout_batch_device(state, actions, n_sims, seed, node_id=0, sim_offset=0, 
     s0, s1 = shard_range(n_sims, rank, world)
     dev = torch.device("cuda", torch.cuda.current_device())
     hist = torch.zeros((len(actions), state.players), dtype=torch.int64, device=dev)
+    cur = torch.cuda.current_stream(dev)
+    if stream is not None:
+        stream.wait_stream(cur)          # the kernel adds into hist after its zero fill
     if s1 > s0:
         dvc.rollout_batch_async(state, actions, seed, node_id, sim_offset + s0, sim_offset + s1, hist,
                                 stream=stream, crn=crn)
     if stream is not None:
         # the all_reduce (and a gloo host copy) run on torch's current stream:
         # order them after the kernel on the caller's stream
-        torch.cuda.current_stream(dev).wait_stream(stream)
+        cur.wait_stream(stream)
     return merge_hist(hist, group)
 
 
