@@ -32,6 +32,9 @@ namespace dvc {
 // registers, +1.4%; consecutive = 0 -1.1%), four players jokerless
 // consecutive = 0 2 (+0.6%; consecutive -3.1%); otherwise 3 (C4 -0.1% /
 // -0.4% at 4 / 2).
+#ifndef DVC_STEPS3
+#define DVC_STEPS3 1   // two-player jokerless consecutive: a third nested decision step per loop iteration
+#endif
 #ifndef DVC_REFILL_MINB2
 #define DVC_REFILL_MINB2 4
 #endif
@@ -382,6 +385,15 @@ __global__ void __launch_bounds__(256, refill_minb(P, JOK, CONS))
                                               kp.path_len);
           ++c1;
           fin = st == FINISH || (PATH && st == VOID);
+          // consecutive rules (longer turns): a third step nested in the
+          // second, +0.2% on c2_d1, +1.1..2.2% on five other C2 deals, -3.8%
+          // on the 4-action endgame c2_d8; consecutive = 0 -5% (§M)
+          if (DVC_STEPS3 && CONS && !fin) {
+            st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
+                                                kp.path_len);
+            ++c1;
+            fin = st == FINISH || (PATH && st == VOID);
+          }
         }
         if (fin) {
           record<MODE>(sm, kp, P, a, s, outcome<P, PATH>(S, st, kp));
