@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(1024) rollout_naive_kernel(const __grid_consta
 // applied) in shared memory.  Whenever the ring holds fewer than 32, the whole
 // warp -- converged -- takes 32 new work items and starts them (Philox block D,
 // table lookup, root action), pushing the ones still running.  The main loop is
-// two decision steps for every lane; a lane whose playout ends records the
+// two (two-player jokerless consecutive: three) nested decision steps for
+// every lane; a lane whose playout ends records the
 // winner and pops the next started playout from the ring in the same
 // iteration, so lanes never idle on playout-length variance and the start
 // code never runs with a handful of lanes (BASELINE.json north_star: lanes
@@ -370,7 +371,8 @@ __global__ void __launch_bounds__(256, refill_minb(P, JOK, CONS))
     // through the second): the ballot / pop / produce checks are paid once
     // per two steps.  DESIGN.md §M: +4.2% C2, +2.4% C4, +6% 2p jokers over one
     // step; two flat `if (active)` blocks measured +2.8%, three steps 0%,
-    // four -2%.
+    // four -2% (round 1).  Round 2: three steps in the two-player jokerless
+    // consecutive kernel (+0.2..2.2% on C2 deals), not elsewhere.
     if (active) {
       st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                           kp.path_len);
