@@ -32,6 +32,9 @@ namespace dvc {
 // registers, +1.4%; consecutive = 0 -1.1%), four players jokerless
 // consecutive = 0 2 (+0.6%; consecutive -3.1%); otherwise 3 (C4 -0.1% /
 // -0.4% at 4 / 2).
+#ifndef DVC_REC1_2J
+#define DVC_REC1_2J 1   // the two-player joker kernel under consecutive rules records once per iteration too
+#endif
 #ifndef DVC_STEPS3
 #define DVC_STEPS3 1   // two-player jokerless consecutive: a third nested decision step per loop iteration
 #endif
@@ -377,10 +380,11 @@ __global__ void __launch_bounds__(256, refill_minb(P, JOK, CONS))
       st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                           kp.path_len);
       ++c1;
-      if constexpr (P == 2 && !JOK) {
+      if constexpr (P == 2 && (!JOK || (DVC_REC1_2J && CONS))) {
         // one record site per iteration: a lane that finishes in the first
         // step skips the second and records after it (one divergent region
-        // instead of two): +0.6% on C2; the other instantiations -0.1% (§M)
+        // instead of two): +0.6% on C2, +0.4% on C3; 2p jokers consecutive = 0
+        // -0.5%, 3-4 players -0.1% (§M)
         bool fin = st == FINISH || (PATH && st == VOID);   // VOID exists in path batches only
         if (!fin) {
           st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(256, refill_minb(P, JOK, CONS))
           // consecutive rules (longer turns): a third step nested in the
           // second, +0.2% on c2_d1, +1.1..2.2% on five other C2 deals, -3.8%
           // on the 4-action endgame c2_d8; consecutive = 0 -5% (§M)
-          if (DVC_STEPS3 && CONS && !fin) {
+          if (DVC_STEPS3 && CONS && !JOK && !fin) {
             st = step_block<P, JOK, CONS, MODE, DVC_LUT_KIND(P, JOK, CONS)>(S, st, philox_rk(s, c1, kp), c1 & 63u, sm.meta, sm.path, a, kp,
                                                 kp.path_len);
             ++c1;
